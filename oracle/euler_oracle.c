@@ -1,0 +1,212 @@
+/*
+ * CPU oracle in C - TEST INFRASTRUCTURE ONLY (the checker and the timed CPU
+ * baseline of bench.py; never linked into the product library).  Threads are
+ * plain pthreads over contiguous element ranges (the image has no libgomp).
+ *
+ * A line-for-line restatement of oracle/euler_oracle.py (which is pinned
+ * bitwise to the reference sumfac 0.1.0 by tests/golden/euler_cartesian.npz)
+ * in plain C, so that bench.py can time the reference algorithm on the GPU
+ * box's host cores with every thread it has:
+ *
+ *   euler_volume_cartesian   R = scale sum_j sum_l D[r_j,l] F#_j(u_r, u_r(j->l))
+ *     - products D*F rounded separately (kernel.py:244), summed over l in
+ *       numpy's ndarray.sum order (kernel.py:264), then over j
+ *       (burgers.py:131); compile with -ffp-contract=off so no FMA is formed;
+ *   hadamard_rowsum_batched  out[e,R] = sum_j sum_l B[j,R,l] F[e,j,R,l]
+ *     (kernel.py:244,264 + burgers.py:131), the config-2 reference pipeline.
+ *
+ * Logarithms come from libm, which may differ from numpy's SIMD log in the
+ * last bit: agreement with the Python oracle is ~1e-15 relative, not bitwise.
+ */
+#include <math.h>
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define LOGMEAN_EPS 1.0e-4
+
+static double logmean(double x, double y, double lx, double ly) {
+  double d = y - x;
+  double s = x + y;
+  if (d * d < LOGMEAN_EPS * s * s) {
+    double u = (d * d) / (s * s);
+    return s / (2.0 + u * (2.0 / 3.0 + u * (2.0 / 5.0 + u * (2.0 / 7.0))));
+  }
+  return d / (ly - lx);
+}
+
+typedef struct {
+  double rho, v[3], p, beta, vv, lr, lb;
+} node_t;
+
+/* flux component vector for direction j (Cartesian unit normal e_j) */
+static void chandrashekar(const node_t* a, const node_t* b, int j, double gamma, double f[5]) {
+  double rho_ln = logmean(a->rho, b->rho, a->lr, b->lr);
+  double beta_ln = logmean(a->beta, b->beta, a->lb, b->lb);
+  double vbar[3];
+  for (int m = 0; m < 3; ++m) vbar[m] = 0.5 * (a->v[m] + b->v[m]);
+  double rho_bar = 0.5 * (a->rho + b->rho);
+  double beta_bar = 0.5 * (a->beta + b->beta);
+  double p_hat = rho_bar / (2.0 * beta_bar);
+  double nrm[3] = {j == 0 ? 1.0 : 0.0, j == 1 ? 1.0 : 0.0, j == 2 ? 1.0 : 0.0};
+  double vn = vbar[0] * nrm[0] + vbar[1] * nrm[1] + vbar[2] * nrm[2];
+  double f1 = rho_ln * vn;
+  double fm[3];
+  for (int m = 0; m < 3; ++m) fm[m] = f1 * vbar[m] + p_hat * nrm[m];
+  double half_v2 = 0.25 * (a->vv + b->vv);
+  double f5 = f1 * (1.0 / (2.0 * (gamma - 1.0) * beta_ln) - half_v2) +
+              (vbar[0] * fm[0] + vbar[1] * fm[1] + vbar[2] * fm[2]);
+  f[0] = f1;
+  f[1] = fm[0];
+  f[2] = fm[1];
+  f[3] = fm[2];
+  f[4] = f5;
+}
+
+/* numpy ndarray.sum(axis=-1) order over t[0..n-1] (n <= 128 here) */
+static double numpy_sum(const double* t, int n) {
+  if (n < 8) {
+    double acc = 0.0;
+    for (int i = 0; i < n; ++i) acc = acc + t[i];
+    return acc;
+  }
+  double r[8];
+  for (int q = 0; q < 8; ++q) r[q] = t[q];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
+    for (int q = 0; q < 8; ++q) r[q] = r[q] + t[i + q];
+  double acc = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; i < n; ++i) acc = acc + t[i];
+  return acc;
+}
+
+static void element_volume(int n, const double* D, double gamma, double scale, const double* U,
+                           double* R, node_t* nd, double* terms) {
+  const int nodes = n * n * n;
+  for (int r = 0; r < nodes; ++r) {
+    node_t* q = &nd[r];
+    q->rho = U[r];
+    for (int m = 0; m < 3; ++m) q->v[m] = U[(1 + m) * nodes + r] / q->rho;
+    q->vv = q->v[0] * q->v[0] + q->v[1] * q->v[1] + q->v[2] * q->v[2];
+    q->p = (gamma - 1.0) * (U[4 * nodes + r] - 0.5 * q->rho * q->vv);
+    q->beta = q->rho / (2.0 * q->p);
+    q->lr = log(q->rho);
+    q->lb = log(q->beta);
+  }
+  for (int r = 0; r < nodes; ++r) {
+    double total[5] = {0, 0, 0, 0, 0};
+    int stride = 1;
+    for (int j = 0; j < 3; ++j) {
+      int rj = (r / stride) % n;
+      /* terms[v * n + l] = D[rj, l] * F_v(u_r, u_r(j->l)) */
+      for (int l = 0; l < n; ++l) {
+        double f[5];
+        chandrashekar(&nd[r], &nd[r + (l - rj) * stride], j, gamma, f);
+        for (int v = 0; v < 5; ++v) terms[v * n + l] = D[rj * n + l] * f[v];
+      }
+      for (int v = 0; v < 5; ++v) {
+        double s = numpy_sum(&terms[v * n], n);
+        total[v] = (j == 0) ? s : total[v] + s;
+      }
+      stride *= n;
+    }
+    for (int v = 0; v < 5; ++v) R[v * nodes + r] = scale * total[v];
+  }
+}
+
+/* ---- tiny static-partition parallel-for over elements -------------------- */
+typedef struct {
+  void (*body)(void* ctx, int64_t e0, int64_t e1);
+  void* ctx;
+  int64_t e0, e1;
+} range_t;
+
+static void* range_main(void* arg) {
+  range_t* r = (range_t*)arg;
+  if (r->e1 > r->e0) r->body(r->ctx, r->e0, r->e1);
+  return NULL;
+}
+
+static void parallel_for(int64_t E, int threads, void (*body)(void*, int64_t, int64_t),
+                         void* ctx) {
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  if (threads == 1 || E < 2) {
+    body(ctx, 0, E);
+    return;
+  }
+  pthread_t tid[256];
+  range_t rg[256];
+  int64_t chunk = (E + threads - 1) / threads;
+  for (int t = 0; t < threads; ++t) {
+    rg[t].body = body;
+    rg[t].ctx = ctx;
+    rg[t].e0 = t * chunk < E ? t * chunk : E;
+    rg[t].e1 = (t + 1) * chunk < E ? (t + 1) * chunk : E;
+    pthread_create(&tid[t], NULL, range_main, &rg[t]);
+  }
+  for (int t = 0; t < threads; ++t) pthread_join(tid[t], NULL);
+}
+
+typedef struct {
+  int n;
+  const double *D, *U;
+  double gamma, scale, *R;
+} euler_ctx_t;
+
+static void euler_body(void* arg, int64_t e0, int64_t e1) {
+  euler_ctx_t* c = (euler_ctx_t*)arg;
+  const int n = c->n, nodes = n * n * n;
+  node_t* nd = (node_t*)malloc(sizeof(node_t) * nodes);
+  double* terms = (double*)malloc(sizeof(double) * 5 * n);
+  for (int64_t e = e0; e < e1; ++e)
+    element_volume(n, c->D, c->gamma, c->scale, c->U + e * 5 * nodes, c->R + e * 5 * nodes, nd,
+                   terms);
+  free(nd);
+  free(terms);
+}
+
+int oracle_euler_volume_cartesian(int64_t E, int n, const double* D, double gamma, double scale,
+                                  const double* U, double* R, int threads) {
+  if (n < 2 || n > 16) return 1;
+  euler_ctx_t c = {n, D, U, gamma, scale, R};
+  parallel_for(E, threads, euler_body, &c);
+  return 0;
+}
+
+typedef struct {
+  int64_t R;
+  int n, d;
+  const double *basis, *F;
+  double* out;
+} had_ctx_t;
+
+static void had_body(void* arg, int64_t e0, int64_t e1) {
+  had_ctx_t* c = (had_ctx_t*)arg;
+  const int n = c->n, d = c->d;
+  const int64_t R = c->R;
+  double* t = (double*)malloc(sizeof(double) * n);
+  for (int64_t e = e0; e < e1; ++e) {
+    for (int64_t row = 0; row < R; ++row) {
+      double acc = 0.0;
+      for (int j = 0; j < d; ++j) {
+        const double* f = c->F + ((e * d + j) * R + row) * n;
+        const double* b = c->basis + ((int64_t)j * R + row) * n;
+        for (int l = 0; l < n; ++l) t[l] = b[l] * f[l];
+        double s = numpy_sum(t, n);
+        acc = (j == 0) ? s : acc + s;
+      }
+      c->out[e * R + row] = acc;
+    }
+  }
+  free(t);
+}
+
+int oracle_hadamard_rowsum_batched(int64_t E, int64_t R, int n, int d, const double* basis,
+                                   const double* F, double* out_sum, int threads) {
+  if (n < 1 || n > 128) return 1;
+  had_ctx_t c = {R, n, d, basis, F, out_sum};
+  parallel_for(E, threads, had_body, &c);
+  return 0;
+}

@@ -1,0 +1,68 @@
+// Shared helpers for the sm_100a sum-factorized Hadamard / flux-differencing kernels.
+//
+// Conventions:
+//  * node flat index r = r0 + r1*n + r2*n^2 (x fastest), as in the reference's
+//    indexing.py:1-10; direction j has stride n^j.
+//  * every entry point is stream-ordered on the caller's cudaStream_t, never
+//    allocates, never synchronises, and reports errors through sfb_last_error().
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/sumfac_b200.h"
+
+namespace sfb {
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int check_launch(const char* what);
+
+constexpr int kNumSMs = 148;  // B200; only used as a grid-size hint (the
+                              // runtime value is queried once and cached).
+int num_sms();
+
+// ---------------------------------------------------------------------------
+// FP64 helpers
+// ---------------------------------------------------------------------------
+
+// MUFU.RCP64H seed (about 2^-23 relative) refined by one cubic Newton step
+// (e = 1 - x r; r += r (e + e^2)): ~2^-66 before rounding, i.e. within an ulp
+// or two of the correctly rounded reciprocal.  Used where the quotient feeds
+// a 1e-12-parity result and never a branch decision.
+__device__ __forceinline__ double rcp_approx(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return r;
+}
+
+__device__ __forceinline__ double rcp_refined(double x) {
+  double r = rcp_approx(x);
+  double e = fma(-x, r, 1.0);
+  double e2 = fma(e, e, e);
+  return fma(r, e2, r);
+}
+
+// Stream-lined load of read-once data: bypass L1 allocation.
+__device__ __forceinline__ double2 ld_stream_d2(const double* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void st_stream_d2(double* p, double2 v) {
+  asm volatile("st.global.L1::no_allocate.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y)
+               : "memory");
+}
+
+__host__ __device__ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
+
+}  // namespace sfb
+
+#define SFB_CHECK_ARG(cond, msg)                    \
+  do {                                              \
+    if (!(cond)) return ::sfb::fail(SFB_EINVAL, msg); \
+  } while (0)

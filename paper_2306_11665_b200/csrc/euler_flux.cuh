@@ -1,0 +1,88 @@
+// Chandrashekar entropy-conservative two-point flux for the 3-D compressible
+// Euler equations, in the node-record form used by the sm_100a kernels.
+//
+// Definition (oracle/euler_oracle.py:chandrashekar_flux is
+// the CPU restatement it must match to 1e-12):
+//   rho_ln = L(rho_a, rho_b),  beta = rho / (2 p),  beta_ln = L(beta_a, beta_b)
+//   vbar = (v_a + v_b)/2,  p_hat = rhobar / (2 betabar)
+//   F1 = rho_ln vbar.n ;  F_{1+m} = F1 vbar_m + p_hat n_m
+//   F5 = F1 (1/(2(gamma-1) beta_ln) - (|v_a|^2 + |v_b|^2)/4) + sum_m vbar_m F_{1+m}
+// with L the logarithmic mean:
+//   d = y - x, s = x + y;  if d*d < EPS*s*s:  L = s / (2 + u(2/3 + u(2/5 + u 2/7))), u = d^2/s^2
+//                          else:              L = d / (ln y - ln x)
+// The branch test is evaluated with the same IEEE operations (no FMA) as the
+// oracle, so both always take the same branch.  The kernel works on the halved
+// quantities x/2 (exact scaling), uses per-node logarithms and folds the three
+// per-pair reciprocals (1/L_rho, L_beta, 1/(2 betabar)) into one refined
+// reciprocal; these change rounding only (few ulps), never the branch.
+#pragma once
+
+#include "common.cuh"
+
+namespace sfb {
+
+constexpr double kLogMeanEps = 1.0e-4;
+
+// Per-node record, all entries pre-scaled so that pair sums are exact means.
+struct NodeRec {
+  double hr;       // rho / 2
+  double hv0, hv1, hv2;  // v / 2
+  double hb;       // beta / 2
+  double hlr;      // ln(rho) / 2
+  double hlb;      // ln(beta) / 2
+  double q;        // |v|^2 / 4
+};
+
+// Numerator / denominator of the log mean of (x, y) = (2 hx, 2 hy):
+//   L = num / den.  Series when d^2 < EPS s^2 (tested on halved values; the
+//   test is scale-invariant under exact halving).
+__device__ __forceinline__ void logmean_parts(double hx, double hy, double hlx, double hly,
+                                              double& num, double& den) {
+  double d = __dsub_rn(hy, hx);
+  double s = __dadd_rn(hx, hy);
+  double d2 = __dmul_rn(d, d);
+  double s2 = __dmul_rn(s, s);
+  bool series = d2 < __dmul_rn(__dmul_rn(kLogMeanEps, s), s);
+  // series: L = s/(1 + u(1/3 + u(1/5 + u/7))) on the halved s (== (2s)/(2+...)).
+  // u enters at O(u) only; the refined reciprocal keeps it within ~1e-16.
+  double u = d2 * rcp_refined(s2);
+  num = series ? s : d;
+  den = series ? fma(u, fma(u, fma(u, 1.0 / 7.0, 1.0 / 5.0), 1.0 / 3.0), 1.0)
+               : __dsub_rn(hly, hlx);
+}
+
+// Two-point flux between node records a and b for the (unnormalised)
+// direction vector (n0, n1, n2).  Output f[5].
+__device__ __forceinline__ void chandrashekar(const NodeRec& a, const NodeRec& b, double n0,
+                                              double n1, double n2, double c_gamma,
+                                              double f[5]) {
+  double vb0 = a.hv0 + b.hv0;
+  double vb1 = a.hv1 + b.hv1;
+  double vb2 = a.hv2 + b.hv2;
+  double nr, dr, nb, db;
+  logmean_parts(a.hr, b.hr, a.hlr, b.hlr, nr, dr);  // rho_ln = nr/dr
+  logmean_parts(a.hb, b.hb, a.hlb, b.hlb, nb, db);  // beta_ln = nb/db
+  double sr = a.hr + b.hr;                          // rhobar
+  double sb = a.hb + b.hb;                          // betabar
+  // one reciprocal for 1/dr, 1/nb, 1/sb
+  double p1 = dr * nb;
+  double rr = rcp_refined(p1 * sb);
+  double inv_sb = rr * p1;
+  double t = rr * sb;
+  double inv_dr = t * nb;
+  double inv_nb = t * dr;
+  double rho_ln = nr * inv_dr;
+  double ibeta = db * inv_nb;       // 1 / beta_ln
+  double phat = 0.5 * sr * inv_sb;  // rhobar / (2 betabar)
+  double vn = fma(vb2, n2, fma(vb1, n1, vb0 * n0));
+  double f1 = rho_ln * vn;
+  f[0] = f1;
+  f[1] = fma(f1, vb0, phat * n0);
+  f[2] = fma(f1, vb1, phat * n1);
+  f[3] = fma(f1, vb2, phat * n2);
+  double vv = fma(vb2, vb2, fma(vb1, vb1, vb0 * vb0));
+  double g = fma(c_gamma, ibeta, vv - (a.q + b.q));
+  f[4] = fma(f1, g, phat * vn);
+}
+
+}  // namespace sfb

