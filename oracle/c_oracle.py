@@ -19,8 +19,12 @@ def build():
 def _load():
     global _lib
     if _lib is None:
-        if not os.path.exists(_LIB_PATH):
-            build()
+        if not os.path.exists(_LIB_PATH) or os.access(os.path.join(_HERE, "Makefile"), os.W_OK):
+            try:
+                build()  # make is a no-op when the library is current
+            except Exception:
+                if not os.path.exists(_LIB_PATH):
+                    raise
         lib = ctypes.CDLL(_LIB_PATH)
         p, i64, i, d = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
         lib.oracle_euler_volume_cartesian.argtypes = [i64, i, p, d, d, p, p, i]

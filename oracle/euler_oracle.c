@@ -29,7 +29,7 @@
 static double logmean(double x, double y, double lx, double ly) {
   double d = y - x;
   double s = x + y;
-  if (d * d < LOGMEAN_EPS * s * s) {
+  if (d * d < LOGMEAN_EPS * (s * s)) {
     double u = (d * d) / (s * s);
     return s / (2.0 + u * (2.0 / 3.0 + u * (2.0 / 5.0 + u * (2.0 / 7.0))));
   }

@@ -8,21 +8,28 @@
 // row-summed, summed over directions) for a 5-variable state with the
 // Chandrashekar flux.  The reference evaluates it as pattern -> operand
 // gather -> hadamard_evaluate -> hadamard_row_sum (kernel.py:195-266); here the
-// whole chain is one kernel and nothing but U and R touches HBM:
+// whole chain is one persistent kernel and only U and R touch HBM.
 //
-//   stage 0  the CTA's EPB elements (EPB*5*N^3 doubles, contiguous) are
-//            streamed into shared memory with 16-byte coalesced loads;
-//   stage 1  one thread per node: primitives, per-node logarithms (ln rho,
-//            ln beta), the node record of euler_flux.cuh, and the diagonal
-//            term sum_j D[r_j,r_j] f_j(u_r) (written as the initial residual);
-//   stage 2  one thread per (element, direction, line): the line's N node
-//            records in registers, each symmetric pair (a<b) evaluated ONCE
-//            and scattered to both rows (D[a,b] and D[b,a]) - the
-//            n(n-1)/2-per-line sum factorization of Theorem 1, halved again by
-//            symmetry; warps are direction-uniform by construction;
-//   stage 3  direction-ordered accumulation into the shared residual (three
-//            barrier-separated phases; deterministic order, no atomics);
-//   stage 4  coalesced 16-byte stores of the residual.
+// Per CTA, loop over blocks of EPB elements (grid = resident CTAs):
+//   prefetch  one elected thread streams the NEXT block (EPB*5*N^3 doubles,
+//             contiguous) into the other half of a double buffer with a 1-D
+//             bulk copy (cp.async.bulk -> UBLKCP) completing on an mbarrier,
+//             so HBM traffic overlaps the FP64 work of the current block;
+//   stage 1   one thread per node: primitives, per-node logarithms, the node
+//             record of euler_flux.cuh, and the diagonal term
+//             sum_j D[r_j,r_j] f_j(u_r) (the residual's initial value);
+//   stage 2   one thread per (element, direction, line), warp-uniform in the
+//             direction (template DIR): each symmetric pair a<b of the line is
+//             evaluated ONCE and scattered to both rows with D[a,b], D[b,a]
+//             (Theorem 1's n(n-1)/2 per line, halved by symmetry);
+//   stage 3   direction-ordered accumulation into the shared residual
+//             (barrier-separated phases: deterministic, no atomics);
+//   stage 4   coalesced 16-byte streaming stores of the residual.
+// Node records and the residual use a plane-rotation swizzle
+//   pos(r0,r1,r2) = r2 N^2 + ((r0+r2) mod N) + N ((r1+r2) mod N)
+// which makes the stride-1, stride-N and stride-N^2 line accesses of all three
+// directions bank-conflict free for N = 4.
+#include "bulk.cuh"
 #include "common.cuh"
 #include "euler_flux.cuh"
 
@@ -37,154 +44,328 @@ template <int N>
 struct EulerCartCfg {
   static constexpr int kNodes = N * N * N;
   static constexpr int kLines = N * N;
-  // elements per CTA: keep EPB*N^2 a multiple of 32 where affordable so that
-  // every warp works on one direction
-  static constexpr int kEPB = (N == 2) ? 16 : (N == 3) ? 8 : (N == 4) ? 4 : (N == 5) ? 2 : 1;
-  static constexpr int kThreads = 3 * kLines * kEPB;
-  static constexpr int kRecs = 8;
-  static constexpr size_t kSmem =
-      (size_t)kEPB * kNodes * (kRecs + 5) * sizeof(double);
+  // elements per block; line threads = 3 EPB N^2 (padded to warps), chosen so
+  // the padding is small and the line warps are direction-uniform for N = 4
+  static constexpr int kEPB = (N == 2) ? 8 : (N == 3) ? 7 : (N == 7 || N == 8) ? 1 : 2;
+  static constexpr int kLineThreads = 3 * kLines * kEPB;
+  static constexpr int kLineWarps = (kLineThreads + 31) / 32;
+  // prep warps balance node preprocessing + stores against the line work
+  static constexpr int kPrepWarps = (N <= 3) ? 3 : 1;
+  static constexpr int kThreads = 32 * (kLineWarps + kPrepWarps);
+  static constexpr int kMinBlocks = (N == 4) ? 4 : 1;
+  static constexpr int kVals = kEPB * 5 * kNodes;  // doubles per block of states
+  static constexpr int kPlanes = 13;               // 8 record planes + 5 diagonal planes
+  static constexpr int kRecVals = kPlanes * kEPB * kNodes;
+  // smem (doubles): 2 input buffers + 2 record sets + 3 direction residuals + diag(D)
+  static constexpr size_t kSmem = (size_t)(2 * kVals + 2 * kRecVals + 3 * kVals + 8) * sizeof(double);
+  static constexpr bool kBulk = ((kVals * 8) % 16) == 0;
 };
 
 template <int N>
-__global__ void __launch_bounds__(EulerCartCfg<N>::kThreads)
+__device__ __forceinline__ int swz(int r0, int r1, int r2) {
+  int a = r0 + r2;
+  a = a >= N ? a - N : a;
+  int b = r1 + r2;
+  b = b >= N ? b - N : b;
+  return r2 * N * N + a + N * b;
+}
+
+template <int N>
+__device__ __forceinline__ int swz_flat(int r) {
+  return swz<N>(r % N, (r / N) % N, r / (N * N));
+}
+
+// Cartesian Chandrashekar flux along direction dir (unit normal e_dir).  The
+// direction only selects operands (ALU selects), so one code path serves all
+// three directions and warps never diverge on it.
+__device__ __forceinline__ void chandrashekar_cart(const NodeRec& a, const NodeRec& b, int dir,
+                                                   double c_gamma, double f[5]) {
+  const double vb0 = a.hv0 + b.hv0;
+  const double vb1 = a.hv1 + b.hv1;
+  const double vb2 = a.hv2 + b.hv2;
+  double nr, dr, nb, db;
+  logmean_parts(a.hr, b.hr, a.hlr, b.hlr, nr, dr);  // rho_ln  = nr / dr
+  logmean_parts(a.hb, b.hb, a.hlb, b.hlb, nb, db);  // beta_ln = nb / db
+  const double sr = a.hr + b.hr;                    // rhobar
+  const double sb = a.hb + b.hb;                    // betabar
+  const double p1 = dr * nb;
+  const double rr = rcp_refined(p1 * sb);
+  const double inv_sb = rr * p1;
+  const double t = rr * sb;
+  const double rho_ln = nr * (t * nb);
+  const double ibeta = db * (t * dr);
+  const double phat = 0.5 * sr * inv_sb;
+  const double vn = dir == 0 ? vb0 : (dir == 1 ? vb1 : vb2);
+  const double f1 = rho_ln * vn;
+  f[0] = f1;
+  f[1] = fma(f1, vb0, dir == 0 ? phat : 0.0);
+  f[2] = fma(f1, vb1, dir == 1 ? phat : 0.0);
+  f[3] = fma(f1, vb2, dir == 2 ? phat : 0.0);
+  const double vv = fma(vb2, vb2, fma(vb1, vb1, vb0 * vb0));
+  const double g = fma(c_gamma, ibeta, vv - (a.q + b.q));
+  f[4] = fma(f1, g, phat * vn);
+}
+
+// Pair order of one line: the circle-method round robin, so consecutive pairs
+// are disjoint (independent dependency chains and accumulators) - for N = 4:
+// (0,3)(1,2) (1,3)(0,2) (2,3)(0,1).
+template <int N>
+struct PairOrder {
+  static constexpr int kPairs = N * (N - 1) / 2;
+  int a[kPairs > 0 ? kPairs : 1], b[kPairs > 0 ? kPairs : 1];
+  constexpr PairOrder() : a{}, b{} {
+    const int M = (N % 2 == 0) ? N : N + 1;  // odd N: dummy node M-1
+    int k = 0;
+    for (int round = 0; round < M - 1; ++round) {
+      for (int i = 0; i < M / 2; ++i) {
+        int x = (i == 0) ? M - 1 : (round + i) % (M - 1);
+        int y = (round - i + (M - 1)) % (M - 1);
+        if (i == 0) y = round;
+        if (x >= N || y >= N) continue;
+        a[k] = x < y ? x : y;
+        b[k] = x < y ? y : x;
+        ++k;
+      }
+    }
+  }
+};
+
+template <int N>
+struct LineOut {
+  int pos[N];
+  double acc[N][5];
+};
+
+template <int N>
+__device__ __forceinline__ void line_work(const double* __restrict__ rec, int el, int dir, int L,
+                                          const DMat<N>& Dm, double c_gamma, LineOut<N>& o) {
+  using Cfg = EulerCartCfg<N>;
+  constexpr int NN = Cfg::kNodes;
+  constexpr int S = Cfg::kEPB * NN;  // record-plane stride
+  const int u = L % N, w = L / N;
+#pragma unroll
+  for (int a = 0; a < N; ++a) {
+    const int r0 = dir == 0 ? a : u;
+    const int r1 = dir == 1 ? a : (dir == 0 ? u : w);
+    const int r2 = dir == 2 ? a : w;
+    o.pos[a] = swz<N>(r0, r1, r2);
+  }
+  const double* re = rec + el * NN;
+  auto load = [&](int a) {
+    NodeRec q;
+    const double* p = re + o.pos[a];
+    q.hr = p[0];
+    q.hv0 = p[S];
+    q.hv1 = p[2 * S];
+    q.hv2 = p[3 * S];
+    q.hb = p[4 * S];
+    q.hlr = p[5 * S];
+    q.hlb = p[6 * S];
+    q.q = p[7 * S];
+    return q;
+  };
+#pragma unroll
+  for (int a = 0; a < N; ++a)
+#pragma unroll
+    for (int v = 0; v < 5; ++v) o.acc[a][v] = 0.0;
+  constexpr PairOrder<N> po;
+#pragma unroll
+  for (int k = 0; k < PairOrder<N>::kPairs; ++k) {
+    const int a = po.a[k], b = po.b[k];
+    const NodeRec ra = load(a);
+    const NodeRec rb = load(b);
+    double f[5];
+    chandrashekar_cart(ra, rb, dir, c_gamma, f);
+    const double dab = Dm.d[a * N + b], dba = Dm.d[b * N + a];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      o.acc[a][v] = fma(dab, f[v], o.acc[a][v]);
+      o.acc[b][v] = fma(dba, f[v], o.acc[b][v]);
+    }
+  }
+}
+
+// named barriers (id 0 is __syncthreads)
+__device__ __forceinline__ void nbar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void nbar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// Warp-specialised persistent kernel.  Line warps (the FP64-heavy pair work
+// and the residual stores) and prep warps (bulk prefetch, node records and the
+// diagonal term) run concurrently on consecutive element blocks, handing the
+// double-buffered record sets over through named barriers:
+//   REC_FULL[s]  prep -> line : records + diagonal of the block in set s ready
+//   REC_EMPTY[s] line -> prep : record set s consumed
+template <int N>
+__global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kMinBlocks)
     euler_cartesian_kernel(int64_t E, const DMat<N> Dm, double gm1, double c_gamma,
                            const double* __restrict__ U, double* __restrict__ R) {
   using Cfg = EulerCartCfg<N>;
   constexpr int NN = Cfg::kNodes;
   constexpr int EPB = Cfg::kEPB;
-  constexpr int kVals = EPB * 5 * NN;
-  extern __shared__ double smem[];
-  double* Rs = smem;             // [EPB][5][NN]  (stages U in, R out)
-  double* nd = smem + kVals;     // [8][EPB*NN]   node records, SoA
+  constexpr int kVals = Cfg::kVals;
+  constexpr int S = EPB * NN;
+  constexpr int kLineT = 32 * Cfg::kLineWarps;
+  constexpr int kPrepT = 32 * Cfg::kPrepWarps;
+  constexpr int kAll = kLineT + kPrepT;
+  enum { REC_FULL = 1, REC_EMPTY = 3, LINE_ONLY = 5, PREP_ONLY = 6 };
+  extern __shared__ __align__(16) double smem[];
+  double* ibuf = smem;                      // [2][EPB][5][NN] bulk-copy target
+  double* recb = smem + 2 * kVals;          // [2][13][EPB*NN] swizzled records + diagonal
+  double* resb = recb + 2 * Cfg::kRecVals;  // [3][EPB][5][NN] swizzled direction residuals
+  double* ddiag = resb + 3 * kVals;         // [N] scale*D[i][i]
+  __shared__ uint64_t full[2];
 
   const int tid = threadIdx.x;
-  const int64_t e0 = (int64_t)blockIdx.x * EPB;
-  const int nel = (E - e0) < EPB ? (int)(E - e0) : EPB;
-  const int nvals = nel * 5 * NN;
-  const double* Ub = U + e0 * 5 * NN;
-
-  // ---- stage 0: stream the element block in -------------------------------
-  if constexpr ((kVals % 2) == 0) {
-    for (int i = 2 * tid; i < nvals; i += 2 * Cfg::kThreads) {
-      double2 v = ld_stream_d2(Ub + i);
-      Rs[i] = v.x;
-      Rs[i + 1] = v.y;
-    }
-  } else {
-    for (int i = tid; i < nvals; i += Cfg::kThreads) Rs[i] = __ldcs(Ub + i);
+  const int64_t nblocks = (E + EPB - 1) / EPB;
+  if (tid == 0) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) ddiag[i] = Dm.d[i * N + i];  // static indices: no local copy
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_mbar_init();
   }
   __syncthreads();
+  const int niter = blockIdx.x < nblocks ? (int)((nblocks - 1 - blockIdx.x) / gridDim.x) + 1 : 0;
 
-  // ---- stage 1: node records + diagonal term --------------------------------
-  for (int i = tid; i < EPB * NN; i += Cfg::kThreads) {
-    const int el = i / NN;
-    const int r = i - el * NN;
-    double* u = Rs + el * 5 * NN + r;
-    const double rho = u[0], m0 = u[NN], m1 = u[2 * NN], m2 = u[3 * NN], et = u[4 * NN];
-    const double irho = rcp_refined(rho);
-    const double v0 = m0 * irho, v1 = m1 * irho, v2 = m2 * irho;
-    const double vv = fma(v2, v2, fma(v1, v1, v0 * v0));
-    const double p = gm1 * fma(-0.5 * rho, vv, et);
-    const double beta = 0.5 * rho * rcp_refined(p);
-    nd[0 * EPB * NN + i] = 0.5 * rho;
-    nd[1 * EPB * NN + i] = 0.5 * v0;
-    nd[2 * EPB * NN + i] = 0.5 * v1;
-    nd[3 * EPB * NN + i] = 0.5 * v2;
-    nd[4 * EPB * NN + i] = 0.5 * beta;
-    nd[5 * EPB * NN + i] = 0.5 * log(rho);
-    nd[6 * EPB * NN + i] = 0.5 * log(beta);
-    nd[7 * EPB * NN + i] = 0.25 * vv;
-    const int r0 = r % N, r1 = (r / N) % N, r2 = r / (N * N);
-    const double d0 = Dm.d[r0 * N + r0], d1 = Dm.d[r1 * N + r1], d2 = Dm.d[r2 * N + r2];
-    const double w = fma(d2, v2, fma(d1, v1, d0 * v0));
-    u[0] = rho * w;
-    u[NN] = fma(m0, w, p * d0);
-    u[2 * NN] = fma(m1, w, p * d1);
-    u[3 * NN] = fma(m2, w, p * d2);
-    u[4 * NN] = (et + p) * w;
-  }
-  __syncthreads();
-
-  // ---- stage 2: line threads -------------------------------------------------
-  const int dir = tid / (EPB * Cfg::kLines);  // warp-uniform when EPB*N^2 % 32 == 0
-  const int rem = tid - dir * EPB * Cfg::kLines;
-  const int el = rem / Cfg::kLines;
-  const int L = rem - el * Cfg::kLines;
-  int base, stride;
-  if (dir == 0) {
-    base = L * N;
-    stride = 1;
-  } else if (dir == 1) {
-    base = (L % N) + (L / N) * N * N;
-    stride = N;
-  } else {
-    base = L;
-    stride = N * N;
-  }
-  const int nb = el * NN + base;  // node index of line point 0 in nd
-
-  double acc[N][5];
+  if (tid < kLineT) {
+    // =========================== line warps ==================================
+    const int dir = tid / (EPB * Cfg::kLines);
+    const int rem = tid - dir * EPB * Cfg::kLines;
+    const int el = rem / Cfg::kLines;
+    const int L = rem - el * Cfg::kLines;
+    const bool active = tid < Cfg::kLineThreads;
+    for (int it = 0; it < niter; ++it) {
+      const int s = it & 1;
+      const double* rec = recb + s * Cfg::kRecVals;
+      nbar_sync(REC_FULL + s, kAll);
+      LineOut<N> o;
+      if (active) {
+        line_work<N>(rec, el, dir, L, Dm, c_gamma, o);
+        if (dir == 0) {  // direction 0 also carries the diagonal term
+          const double* dg = rec + 8 * S + el * NN;
 #pragma unroll
-  for (int a = 0; a < N; ++a)
+          for (int a = 0; a < N; ++a)
 #pragma unroll
-    for (int v = 0; v < 5; ++v) acc[a][v] = 0.0;
-
-  auto load_rec = [&](int a) {
-    NodeRec q;
-    const int k = nb + a * stride;
-    q.hr = nd[0 * EPB * NN + k];
-    q.hv0 = nd[1 * EPB * NN + k];
-    q.hv1 = nd[2 * EPB * NN + k];
-    q.hv2 = nd[3 * EPB * NN + k];
-    q.hb = nd[4 * EPB * NN + k];
-    q.hlr = nd[5 * EPB * NN + k];
-    q.hlb = nd[6 * EPB * NN + k];
-    q.q = nd[7 * EPB * NN + k];
-    return q;
-  };
-  const double n0 = dir == 0 ? 1.0 : 0.0;
-  const double n1 = dir == 1 ? 1.0 : 0.0;
-  const double n2 = dir == 2 ? 1.0 : 0.0;
-
-#pragma unroll
-  for (int a = 0; a < N - 1; ++a) {
-    const NodeRec ra = load_rec(a);
-#pragma unroll
-    for (int b = a + 1; b < N; ++b) {
-      const NodeRec rb = load_rec(b);
-      double f[5];
-      chandrashekar(ra, rb, n0, n1, n2, c_gamma, f);
-      const double dab = Dm.d[a * N + b], dba = Dm.d[b * N + a];
-#pragma unroll
-      for (int v = 0; v < 5; ++v) {
-        acc[a][v] = fma(dab, f[v], acc[a][v]);
-        acc[b][v] = fma(dba, f[v], acc[b][v]);
+            for (int v = 0; v < 5; ++v) o.acc[a][v] += dg[v * S + o.pos[a]];
+        }
       }
-    }
-  }
-
-  // ---- stage 3: direction-ordered accumulation ------------------------------
+      nbar_arrive(REC_EMPTY + s, kAll);
+      if (active) {
+        double* rs = resb + dir * kVals + el * 5 * NN;
 #pragma unroll
-  for (int phase = 0; phase < 3; ++phase) {
-    if (dir == phase) {
+        for (int a = 0; a < N; ++a)
 #pragma unroll
-      for (int a = 0; a < N; ++a) {
-        double* rr = Rs + el * 5 * NN + base + a * stride;
-#pragma unroll
-        for (int v = 0; v < 5; ++v) rr[v * NN] += acc[a][v];
+          for (int v = 0; v < 5; ++v) rs[o.pos[a] + v * NN] = o.acc[a][v];
       }
+      nbar_sync(LINE_ONLY, kLineT);  // all three direction residuals written
+      // residual = (R_0 + R_1) + R_2, swizzled smem -> natural global order
+      {
+        const int64_t blk = (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
+        const int64_t e0 = blk * EPB;
+        const int nel = (E - e0) < EPB ? (int)(E - e0) : EPB;
+        const double* r0 = resb;
+        const double* r1 = r0 + kVals;
+        const double* r2 = r1 + kVals;
+        double* Rb = R + e0 * 5 * NN;
+        const int nvals = nel * 5 * NN;
+        if constexpr ((NN % 2) == 0) {
+          for (int i = 2 * tid; i < nvals; i += 2 * kLineT) {
+            const int r = i % NN;
+            const int q0 = i - r + swz_flat<N>(r), q1 = i - r + swz_flat<N>(r + 1);
+            const double x = (r0[q0] + r1[q0]) + r2[q0];
+            const double y = (r0[q1] + r1[q1]) + r2[q1];
+            st_stream_d2(Rb + i, make_double2(x, y));
+          }
+        } else {
+          for (int i = tid; i < nvals; i += kLineT) {
+            const int r = i % NN;
+            const int q = i - r + swz_flat<N>(r);
+            __stcs(Rb + i, (r0[q] + r1[q]) + r2[q]);
+          }
+        }
+      }
+      nbar_sync(LINE_ONLY, kLineT);  // residual buffers free again
     }
-    __syncthreads();
-  }
-
-  // ---- stage 4: stream the residual out --------------------------------------
-  double* Rb = R + e0 * 5 * NN;
-  if constexpr ((kVals % 2) == 0) {
-    for (int i = 2 * tid; i < nvals; i += 2 * Cfg::kThreads)
-      st_stream_d2(Rb + i, make_double2(Rs[i], Rs[i + 1]));
   } else {
-    for (int i = tid; i < nvals; i += Cfg::kThreads) __stcs(Rb + i, Rs[i]);
+    // =========================== prep warps ==================================
+    const int pt = tid - kLineT;
+    auto block_bytes = [&](int64_t blk) {
+      const int64_t e0 = blk * EPB;
+      const int nel = (E - e0) < EPB ? (int)(E - e0) : EPB;
+      return (uint32_t)nel * 5 * NN * 8;
+    };
+    auto bulk_ok = [&](int64_t blk) { return Cfg::kBulk && (block_bytes(blk) % 16) == 0; };
+    auto issue = [&](int64_t blk, int slot) {
+      const uint32_t bytes = block_bytes(blk);
+      mbar_arrive_expect_tx(&full[slot], bytes);
+      bulk_g2s(ibuf + slot * kVals, U + blk * EPB * 5 * NN, bytes, &full[slot]);
+    };
+    int64_t blk = blockIdx.x;
+    if (pt == 0 && niter > 0 && bulk_ok(blk)) issue(blk, 0);
+    uint32_t parity[2] = {0, 0};
+    for (int it = 0; it < niter; ++it, blk += gridDim.x) {
+      const int slot = it & 1;
+      const int s = it & 1;
+      const int64_t e0 = blk * EPB;
+      const int nel = (E - e0) < EPB ? (int)(E - e0) : EPB;
+      double* in = ibuf + slot * kVals;
+      // all prep threads are done reading the other input slot (block it-1)
+      nbar_sync(PREP_ONLY, kPrepT);
+      const int64_t nxt = blk + gridDim.x;
+      if (pt == 0 && it + 1 < niter && bulk_ok(nxt)) {
+        fence_proxy_async_smem();
+        issue(nxt, slot ^ 1);
+      }
+      if (bulk_ok(blk)) {
+        mbar_wait_parity(&full[slot], parity[slot]);
+        parity[slot] ^= 1;
+      } else {  // odd-sized tail: plain loads
+        for (int i = pt; i < nel * 5 * NN; i += kPrepT) in[i] = __ldcs(U + e0 * 5 * NN + i);
+        nbar_sync(PREP_ONLY, kPrepT);
+      }
+      if (it >= 2) nbar_sync(REC_EMPTY + s, kAll);  // record set s read for block it-2
+      double* rec = recb + s * Cfg::kRecVals;
+      constexpr int kPer = (S + kPrepT - 1) / kPrepT;
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const int i = pt + k * kPrepT;
+        if (kPer * kPrepT != S && i >= S) break;
+        const int el = i / NN;
+        const int r = i - el * NN;
+        const double* u = in + el * 5 * NN + r;
+        const double rho = u[0], m0 = u[NN], m1 = u[2 * NN], m2 = u[3 * NN], et = u[4 * NN];
+        const double irho = rcp_refined(rho);
+        const double v0 = m0 * irho, v1 = m1 * irho, v2 = m2 * irho;
+        const double vv = fma(v2, v2, fma(v1, v1, v0 * v0));
+        const double p = gm1 * fma(-0.5 * rho, vv, et);
+        const double beta = 0.5 * rho * rcp_refined(p);
+        const int c0 = r % N, c1 = (r / N) % N, c2 = r / (N * N);
+        const int q = el * NN + swz<N>(c0, c1, c2);
+        rec[q] = 0.5 * rho;
+        rec[S + q] = 0.5 * v0;
+        rec[2 * S + q] = 0.5 * v1;
+        rec[3 * S + q] = 0.5 * v2;
+        rec[4 * S + q] = 0.5 * beta;
+        rec[5 * S + q] = 0.5 * log(rho);
+        rec[6 * S + q] = 0.5 * log(beta);
+        rec[7 * S + q] = 0.25 * vv;
+        // diagonal term sum_j D[r_j,r_j] f_j(u_r) (planes 8..12)
+        const double d0 = ddiag[c0], d1 = ddiag[c1], d2 = ddiag[c2];
+        const double w = fma(d2, v2, fma(d1, v1, d0 * v0));
+        rec[8 * S + q] = rho * w;
+        rec[9 * S + q] = fma(m0, w, p * d0);
+        rec[10 * S + q] = fma(m1, w, p * d1);
+        rec[11 * S + q] = fma(m2, w, p * d2);
+        rec[12 * S + q] = (et + p) * w;
+      }
+      nbar_arrive(REC_FULL + s, kAll);
+    }
+    // match the REC_EMPTY arrivals of the last (up to) two blocks
+    for (int k = niter - 2 > 0 ? niter - 2 : 0; k < niter; ++k) nbar_sync(REC_EMPTY + (k & 1), kAll);
   }
 }
 
@@ -194,18 +375,22 @@ static int launch_euler_cartesian(int64_t E, const double* Dh, double gamma, dou
   using Cfg = EulerCartCfg<N>;
   DMat<N> Dm;
   for (int i = 0; i < N * N; ++i) Dm.d[i] = scale * Dh[i];
-  static bool attr_done = false;
-  if (!attr_done) {
+  static int per_sm = 0;
+  if (per_sm == 0) {
     cudaFuncSetAttribute(euler_cartesian_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Cfg::kSmem);
-    attr_done = true;
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, euler_cartesian_kernel<N>, Cfg::kThreads,
+                                                  Cfg::kSmem);
+    per_sm = b > 0 ? b : 1;
   }
-  const int64_t blocks = (E + Cfg::kEPB - 1) / Cfg::kEPB;
-  if (blocks > 0x7fffffff) return fail(SFB_EINVAL, "too many elements for one launch");
+  const int64_t nblocks = (E + Cfg::kEPB - 1) / Cfg::kEPB;
+  int64_t grid = (int64_t)num_sms() * per_sm;
+  if (grid > nblocks) grid = nblocks;
   const double gm1 = gamma - 1.0;
   const double c_gamma = 1.0 / (2.0 * gm1);
-  euler_cartesian_kernel<N><<<(unsigned)blocks, Cfg::kThreads, Cfg::kSmem, s>>>(E, Dm, gm1, c_gamma,
-                                                                                U, R);
+  euler_cartesian_kernel<N><<<(unsigned)grid, Cfg::kThreads, Cfg::kSmem, s>>>(E, Dm, gm1, c_gamma,
+                                                                               U, R);
   return check_launch("euler_volume_cartesian");
 }
 
@@ -227,9 +412,9 @@ int euler_cartesian_dispatch(int64_t E, int64_t n, const double* D_host, double 
 
 using namespace sfb;
 
-// D is read on the host (it is folded into the kernel's parameter block); the
+// D is a HOST pointer (n x n, folded into the kernel's parameter block); the
 // Python layer passes the host-built operator exactly as the reference builds
-// it (operators.py:136-152).  Here D must be a HOST pointer.
+// it (operators.py:136-152).
 extern "C" int sfb_euler_volume_cartesian(int64_t E, int64_t n, const double* D, double gamma,
                                           double scale, const double* U, double* R,
                                           sfb_stream_t stream) {

@@ -8,7 +8,7 @@
 //   F1 = rho_ln vbar.n ;  F_{1+m} = F1 vbar_m + p_hat n_m
 //   F5 = F1 (1/(2(gamma-1) beta_ln) - (|v_a|^2 + |v_b|^2)/4) + sum_m vbar_m F_{1+m}
 // with L the logarithmic mean:
-//   d = y - x, s = x + y;  if d*d < EPS*s*s:  L = s / (2 + u(2/3 + u(2/5 + u 2/7))), u = d^2/s^2
+//   d = y - x, s = x + y;  if d*d < EPS*(s*s):  L = s / (2 + u(2/3 + u(2/5 + u 2/7))), u = d^2/s^2
 //                          else:              L = d / (ln y - ln x)
 // The branch test is evaluated with the same IEEE operations (no FMA) as the
 // oracle, so both always take the same branch.  The kernel works on the halved
@@ -34,21 +34,26 @@ struct NodeRec {
 };
 
 // Numerator / denominator of the log mean of (x, y) = (2 hx, 2 hy):
-//   L = num / den.  Series when d^2 < EPS s^2 (tested on halved values; the
-//   test is scale-invariant under exact halving).
+//   L = num / den.  Series when d^2 < EPS (s^2) (tested on halved values; the
+//   test is invariant under the exact halving, and uses the oracle's exact
+//   IEEE operations so both take the same branch).
+//   log branch:     num = d,        den = (ln y - ln x)/2       (per-node logs)
+//   series branch:  num = s s^2,    den = s^2 + d^2 Q(u),  Q = 1/3 + u/5 + u^2/7
+// i.e. s / (1 + u Q(u)) scaled by s^2 so that u = d^2/s^2 is only needed
+// inside Q, where a raw MUFU reciprocal (rel. err ~2^-22) costs < 1e-15
+// relative (u < 1e-4).  The final division happens in the caller's combined
+// reciprocal.
 __device__ __forceinline__ void logmean_parts(double hx, double hy, double hlx, double hly,
                                               double& num, double& den) {
-  double d = __dsub_rn(hy, hx);
-  double s = __dadd_rn(hx, hy);
-  double d2 = __dmul_rn(d, d);
-  double s2 = __dmul_rn(s, s);
-  bool series = d2 < __dmul_rn(__dmul_rn(kLogMeanEps, s), s);
-  // series: L = s/(1 + u(1/3 + u(1/5 + u/7))) on the halved s (== (2s)/(2+...)).
-  // u enters at O(u) only; the refined reciprocal keeps it within ~1e-16.
-  double u = d2 * rcp_refined(s2);
-  num = series ? s : d;
-  den = series ? fma(u, fma(u, fma(u, 1.0 / 7.0, 1.0 / 5.0), 1.0 / 3.0), 1.0)
-               : __dsub_rn(hly, hlx);
+  const double d = __dsub_rn(hy, hx);
+  const double s = __dadd_rn(hx, hy);
+  const double d2 = __dmul_rn(d, d);
+  const double s2 = __dmul_rn(s, s);
+  const bool series = d2 < __dmul_rn(kLogMeanEps, s2);
+  const double u = d2 * rcp_approx(s2);
+  const double q = fma(u, fma(u, 1.0 / 7.0, 1.0 / 5.0), 1.0 / 3.0);
+  num = series ? s * s2 : d;
+  den = series ? fma(d2, q, s2) : __dsub_rn(hly, hlx);
 }
 
 // Two-point flux between node records a and b for the (unnormalised)
