@@ -13,7 +13,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsumfac_b200.so")
+LIB_PATH = os.environ.get("SFB_LIB") or os.path.join(_HERE, "libsumfac_b200.so")
 
 SFB_OK = 0
 SFB_EINVAL = 1

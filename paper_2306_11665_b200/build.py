@@ -68,6 +68,23 @@ def _compile(src, verbose):
     return obj
 
 
+def build_variant(out_path, defines):
+    """Build an experimental variant (extra -D flags) into out_path (tools/ sweeps)."""
+    bdir = os.path.join(ROOT, "build", "variant_" + "_".join(d.replace("=", "") for d in defines))
+    os.makedirs(bdir, exist_ok=True)
+    objs = []
+    for src in _sources():
+        obj = os.path.join(bdir, os.path.basename(src)[:-3] + ".o")
+        cmd = [NVCC, *ARCH, *FLAGS, *("-D" + d for d in defines), "-c", src, "-o", obj]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")
+        objs.append(obj)
+    cmd = [NVCC, *ARCH, "-shared", "-o", out_path, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+    subprocess.run(cmd, check=True, capture_output=True)
+    return out_path
+
+
 def build_library(force=False, verbose=False):
     """Compile every csrc/*.cu for sm_100a and link libsumfac_b200.so."""
     os.makedirs(BUILD, exist_ok=True)

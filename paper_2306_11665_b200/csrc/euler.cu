@@ -33,6 +33,13 @@
 #include "common.cuh"
 #include "euler_flux.cuh"
 
+#ifndef SFB_PAIR_BATCH_N4
+#define SFB_PAIR_BATCH_N4 3
+#endif
+#ifndef SFB_MINBLOCKS_N4
+#define SFB_MINBLOCKS_N4 4
+#endif
+
 namespace sfb {
 
 template <int N>
@@ -52,9 +59,9 @@ struct EulerCartCfg {
   // prep warps balance node preprocessing + stores against the line work
   static constexpr int kPrepWarps = (N <= 3) ? 3 : 1;
   static constexpr int kThreads = 32 * (kLineWarps + kPrepWarps);
-  static constexpr int kMinBlocks = (N == 4) ? 4 : 1;
+  static constexpr int kMinBlocks = (N == 4) ? SFB_MINBLOCKS_N4 : 1;
   static constexpr int kVals = kEPB * 5 * kNodes;  // doubles per block of states
-  static constexpr int kPlanes = 13;               // 8 record planes + 5 diagonal planes
+  static constexpr int kPlanes = 9;                // 8 record planes + pressure
   static constexpr int kRecVals = kPlanes * kEPB * kNodes;
   // smem (doubles): 2 input buffers + 2 record sets + 3 direction residuals + diag(D)
   static constexpr size_t kSmem = (size_t)(2 * kVals + 2 * kRecVals + 3 * kVals + 8) * sizeof(double);
@@ -75,35 +82,53 @@ __device__ __forceinline__ int swz_flat(int r) {
   return swz<N>(r % N, (r / N) % N, r / (N * N));
 }
 
-// Cartesian Chandrashekar flux along direction dir (unit normal e_dir).  The
-// direction only selects operands (ALU selects), so one code path serves all
-// three directions and warps never diverge on it.
-__device__ __forceinline__ void chandrashekar_cart(const NodeRec& a, const NodeRec& b, int dir,
-                                                   double c_gamma, double f[5]) {
-  const double vb0 = a.hv0 + b.hv0;
-  const double vb1 = a.hv1 + b.hv1;
-  const double vb2 = a.hv2 + b.hv2;
-  double nr, dr, nb, db;
-  logmean_parts(a.hr, b.hr, a.hlr, b.hlr, nr, dr);  // rho_ln  = nr / dr
-  logmean_parts(a.hb, b.hb, a.hlb, b.hlb, nb, db);  // beta_ln = nb / db
-  const double sr = a.hr + b.hr;                    // rhobar
-  const double sb = a.hb + b.hb;                    // betabar
-  const double p1 = dr * nb;
-  const double rr = rcp_refined(p1 * sb);
-  const double inv_sb = rr * p1;
-  const double t = rr * sb;
-  const double rho_ln = nr * (t * nb);
-  const double ibeta = db * (t * dr);
-  const double phat = 0.5 * sr * inv_sb;
-  const double vn = dir == 0 ? vb0 : (dir == 1 ? vb1 : vb2);
-  const double f1 = rho_ln * vn;
-  f[0] = f1;
-  f[1] = fma(f1, vb0, dir == 0 ? phat : 0.0);
-  f[2] = fma(f1, vb1, dir == 1 ? phat : 0.0);
-  f[3] = fma(f1, vb2, dir == 2 ? phat : 0.0);
-  const double vv = fma(vb2, vb2, fma(vb1, vb1, vb0 * vb0));
-  const double g = fma(c_gamma, ibeta, vv - (a.q + b.q));
-  f[4] = fma(f1, g, phat * vn);
+// Cartesian Chandrashekar flux along direction dir (unit normal e_dir) for K
+// independent pairs at once.  Every statement is written across the K pairs so
+// the instruction stream carries K independent dependency chains: the FP64
+// pipe needs ~4 independent DFMAs in flight per warp to approach its peak
+// (DFMA latency ~9 cycles; tools/peaks/fp64_latency.cu), which warps alone
+// cannot supply.  The direction only selects operands (ALU selects).
+template <int K>
+__device__ __forceinline__ void chandrashekar_cart_k(const NodeRec* const (&A)[K],
+                                                     const NodeRec* const (&B)[K], int dir,
+                                                     double c_gamma, double (&f)[K][5]) {
+  double vb0[K], vb1[K], vb2[K], nr[K], dr[K], nb[K], db[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    vb0[k] = A[k]->hv0 + B[k]->hv0;
+    vb1[k] = A[k]->hv1 + B[k]->hv1;
+    vb2[k] = A[k]->hv2 + B[k]->hv2;
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    logmean_parts(A[k]->hr, B[k]->hr, A[k]->hlr, B[k]->hlr, nr[k], dr[k]);  // rho_ln
+    logmean_parts(A[k]->hb, B[k]->hb, A[k]->hlb, B[k]->hlb, nb[k], db[k]);  // beta_ln
+  }
+  double sr[K], sb[K], p1[K], rr[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    sr[k] = A[k]->hr + B[k]->hr;  // rhobar
+    sb[k] = A[k]->hb + B[k]->hb;  // betabar
+    p1[k] = dr[k] * nb[k];
+    rr[k] = rcp_refined(p1[k] * sb[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const double inv_sb = rr[k] * p1[k];
+    const double t = rr[k] * sb[k];
+    const double rho_ln = nr[k] * (t * nb[k]);
+    const double ibeta = db[k] * (t * dr[k]);
+    const double phat = 0.5 * sr[k] * inv_sb;
+    const double vn = dir == 0 ? vb0[k] : (dir == 1 ? vb1[k] : vb2[k]);
+    const double f1 = rho_ln * vn;
+    f[k][0] = f1;
+    f[k][1] = fma(f1, vb0[k], dir == 0 ? phat : 0.0);
+    f[k][2] = fma(f1, vb1[k], dir == 1 ? phat : 0.0);
+    f[k][3] = fma(f1, vb2[k], dir == 2 ? phat : 0.0);
+    const double vv = fma(vb2[k], vb2[k], fma(vb1[k], vb1[k], vb0[k] * vb0[k]));
+    const double g = fma(c_gamma, ibeta, vv - (A[k]->q + B[k]->q));
+    f[k][4] = fma(f1, g, phat * vn);
+  }
 }
 
 // Pair order of one line: the circle-method round robin, so consecutive pairs
@@ -129,6 +154,10 @@ struct PairOrder {
     }
   }
 };
+
+// pairs evaluated side by side per line thread (ILP knob)
+template <int N>
+constexpr int kPairBatch = (N == 4) ? SFB_PAIR_BATCH_N4 : 2;
 
 template <int N>
 struct LineOut {
@@ -169,18 +198,33 @@ __device__ __forceinline__ void line_work(const double* __restrict__ rec, int el
 #pragma unroll
     for (int v = 0; v < 5; ++v) o.acc[a][v] = 0.0;
   constexpr PairOrder<N> po;
+  constexpr int P = PairOrder<N>::kPairs;
+  constexpr int K = kPairBatch<N>;
+  NodeRec nrec[N];
 #pragma unroll
-  for (int k = 0; k < PairOrder<N>::kPairs; ++k) {
-    const int a = po.a[k], b = po.b[k];
-    const NodeRec ra = load(a);
-    const NodeRec rb = load(b);
-    double f[5];
-    chandrashekar_cart(ra, rb, dir, c_gamma, f);
-    const double dab = Dm.d[a * N + b], dba = Dm.d[b * N + a];
+  for (int a = 0; a < N; ++a) nrec[a] = load(a);
 #pragma unroll
-    for (int v = 0; v < 5; ++v) {
-      o.acc[a][v] = fma(dab, f[v], o.acc[a][v]);
-      o.acc[b][v] = fma(dba, f[v], o.acc[b][v]);
+  for (int k0 = 0; k0 < P; k0 += K) {
+    const NodeRec* A[K];
+    const NodeRec* B[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int kk = (k0 + k < P) ? k0 + k : P - 1;
+      A[k] = &nrec[po.a[kk]];
+      B[k] = &nrec[po.b[kk]];
+    }
+    double f[K][5];
+    chandrashekar_cart_k<K>(A, B, dir, c_gamma, f);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (k0 + k >= P) break;
+      const int a = po.a[k0 + k], b = po.b[k0 + k];
+      const double dab = Dm.d[a * N + b], dba = Dm.d[b * N + a];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        o.acc[a][v] = fma(dab, f[k][v], o.acc[a][v]);
+        o.acc[b][v] = fma(dba, f[k][v], o.acc[b][v]);
+      }
     }
   }
 }
@@ -202,7 +246,8 @@ __device__ __forceinline__ void nbar_arrive(int id, int count) {
 template <int N>
 __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kMinBlocks)
     euler_cartesian_kernel(int64_t E, const DMat<N> Dm, double gm1, double c_gamma,
-                           const double* __restrict__ U, double* __restrict__ R) {
+                           double gam_ratio, const double* __restrict__ U,
+                           double* __restrict__ R) {
   using Cfg = EulerCartCfg<N>;
   constexpr int NN = Cfg::kNodes;
   constexpr int EPB = Cfg::kEPB;
@@ -243,17 +288,7 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
       const double* rec = recb + s * Cfg::kRecVals;
       nbar_sync(REC_FULL + s, kAll);
       LineOut<N> o;
-      if (active) {
-        line_work<N>(rec, el, dir, L, Dm, c_gamma, o);
-        if (dir == 0) {  // direction 0 also carries the diagonal term
-          const double* dg = rec + 8 * S + el * NN;
-#pragma unroll
-          for (int a = 0; a < N; ++a)
-#pragma unroll
-            for (int v = 0; v < 5; ++v) o.acc[a][v] += dg[v * S + o.pos[a]];
-        }
-      }
-      nbar_arrive(REC_EMPTY + s, kAll);
+      if (active) line_work<N>(rec, el, dir, L, Dm, c_gamma, o);
       if (active) {
         double* rs = resb + dir * kVals + el * 5 * NN;
 #pragma unroll
@@ -262,32 +297,40 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
           for (int v = 0; v < 5; ++v) rs[o.pos[a] + v * NN] = o.acc[a][v];
       }
       nbar_sync(LINE_ONLY, kLineT);  // all three direction residuals written
-      // residual = (R_0 + R_1) + R_2, swizzled smem -> natural global order
+      // residual = diag + (R_0 + R_1) + R_2 per node; the diagonal term
+      // sum_j D[r_j,r_j] f_j(u_r) is rebuilt here from the node record
+      // (rho = 2hr, v = 2hv, p, E + p = p gamma/(gamma-1) + 4 hr q)
       {
         const int64_t blk = (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
         const int64_t e0 = blk * EPB;
         const int nel = (E - e0) < EPB ? (int)(E - e0) : EPB;
-        const double* r0 = resb;
-        const double* r1 = r0 + kVals;
-        const double* r2 = r1 + kVals;
         double* Rb = R + e0 * 5 * NN;
-        const int nvals = nel * 5 * NN;
-        if constexpr ((NN % 2) == 0) {
-          for (int i = 2 * tid; i < nvals; i += 2 * kLineT) {
-            const int r = i % NN;
-            const int q0 = i - r + swz_flat<N>(r), q1 = i - r + swz_flat<N>(r + 1);
-            const double x = (r0[q0] + r1[q0]) + r2[q0];
-            const double y = (r0[q1] + r1[q1]) + r2[q1];
-            st_stream_d2(Rb + i, make_double2(x, y));
-          }
-        } else {
-          for (int i = tid; i < nvals; i += kLineT) {
-            const int r = i % NN;
-            const int q = i - r + swz_flat<N>(r);
-            __stcs(Rb + i, (r0[q] + r1[q]) + r2[q]);
-          }
+        const int nn = nel * NN;
+        for (int i = tid; i < nn; i += kLineT) {
+          const int e = i / NN;
+          const int r = i - e * NN;
+          const int c0 = r % N, c1 = (r / N) % N, c2 = r / (N * N);
+          const int qn = swz<N>(c0, c1, c2);
+          const double* rc = rec + e * NN + qn;
+          const double hr = rc[0], h0 = rc[S], h1 = rc[2 * S], h2 = rc[3 * S];
+          const double q = rc[7 * S], p = rc[8 * S];
+          const double d0 = ddiag[c0], d1 = ddiag[c1], d2 = ddiag[c2];
+          const double w = 2.0 * fma(d2, h2, fma(d1, h1, d0 * h0));  // sum_j d_j v_j
+          const double rho = 2.0 * hr;
+          const double rw = rho * w;
+          const double ep = fma(gam_ratio, p, 4.0 * hr * q);  // E + p
+          const double diag[5] = {rw, fma(2.0 * rw, h0, p * d0), fma(2.0 * rw, h1, p * d1),
+                                  fma(2.0 * rw, h2, p * d2), ep * w};
+          const double* r0 = resb + e * 5 * NN + qn;
+          const double* r1 = r0 + kVals;
+          const double* r2 = r1 + kVals;
+#pragma unroll
+          for (int v = 0; v < 5; ++v)
+            __stcs(Rb + e * 5 * NN + v * NN + r,
+                   ((diag[v] + r0[v * NN]) + r1[v * NN]) + r2[v * NN]);
         }
       }
+      nbar_arrive(REC_EMPTY + s, kAll);  // records (incl. p) consumed
       nbar_sync(LINE_ONLY, kLineT);  // residual buffers free again
     }
   } else {
@@ -350,17 +393,10 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
         rec[2 * S + q] = 0.5 * v1;
         rec[3 * S + q] = 0.5 * v2;
         rec[4 * S + q] = 0.5 * beta;
-        rec[5 * S + q] = 0.5 * log(rho);
-        rec[6 * S + q] = 0.5 * log(beta);
+        rec[5 * S + q] = 0.5 * log_pos(rho);
+        rec[6 * S + q] = 0.5 * log_pos(beta);
         rec[7 * S + q] = 0.25 * vv;
-        // diagonal term sum_j D[r_j,r_j] f_j(u_r) (planes 8..12)
-        const double d0 = ddiag[c0], d1 = ddiag[c1], d2 = ddiag[c2];
-        const double w = fma(d2, v2, fma(d1, v1, d0 * v0));
-        rec[8 * S + q] = rho * w;
-        rec[9 * S + q] = fma(m0, w, p * d0);
-        rec[10 * S + q] = fma(m1, w, p * d1);
-        rec[11 * S + q] = fma(m2, w, p * d2);
-        rec[12 * S + q] = (et + p) * w;
+        rec[8 * S + q] = p;
       }
       nbar_arrive(REC_FULL + s, kAll);
     }
@@ -389,8 +425,9 @@ static int launch_euler_cartesian(int64_t E, const double* Dh, double gamma, dou
   if (grid > nblocks) grid = nblocks;
   const double gm1 = gamma - 1.0;
   const double c_gamma = 1.0 / (2.0 * gm1);
-  euler_cartesian_kernel<N><<<(unsigned)grid, Cfg::kThreads, Cfg::kSmem, s>>>(E, Dm, gm1, c_gamma,
-                                                                               U, R);
+  const double gam_ratio = gamma / gm1;  // (E + p) = p gamma/(gamma-1) + rho|v|^2/2
+  euler_cartesian_kernel<N><<<(unsigned)grid, Cfg::kThreads, Cfg::kSmem, s>>>(
+      E, Dm, gm1, c_gamma, gam_ratio, U, R);
   return check_launch("euler_volume_cartesian");
 }
 
