@@ -175,6 +175,17 @@ int sfb_block_sums(const double* x, int64_t count, int64_t block, double* partia
  * v_m ~ U[vlo,vhi], p ~ U[plo,phi], gamma; element ids start at e0. */
 int sfb_generate_euler_states(int64_t E, int64_t e0, int64_t n, uint64_t seed, double gamma,
                               const double* bounds6, double* U, sfb_stream_t stream);
+/* Modal coefficients Uhat (E, 5, n^3) of config 5 (see synth.modal_states):
+ * (amps5[v] 2^-(k0+k1+k2)) (2u - 1), plus means5[v] c0 at mode 0. */
+int sfb_generate_modal_states(int64_t E, int64_t e0, int64_t n, uint64_t seed,
+                              const double* means5, const double* amps5, double c0,
+                              double* Uhat, sfb_stream_t stream);
+/* Metric cofactors Ja (E, 3, 3, n^3) of the warped K^3 lattice (config 5;
+ * synth.metric_cofactors): x = X + amp prod_k sin(2 pi (X_k + phi_mk)),
+ * Ja = adj(dx/dxi).  nodes: host GLL nodes (n).  Device sin/cos: equal to the
+ * host generator to ~1e-15, not bitwise. */
+int sfb_generate_metric(int64_t E, int64_t e0, int64_t n, uint64_t seed, const double* nodes,
+                        int64_t K, double amp, double* Ja, sfb_stream_t stream);
 /* F (E, d, R, n) entries U[lo,hi] on the pattern (config 2). */
 int sfb_generate_uniform(int64_t count, int64_t i0, uint64_t seed, double lo, double hi,
                          double* out, sfb_stream_t stream);

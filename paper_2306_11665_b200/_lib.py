@@ -52,6 +52,8 @@ SIGNATURES = {
     "sfb_block_sums": [_p, _i64, _i64, _p, _p],
     "sfb_generate_euler_states": [_i64, _i64, _i64, _u64, _dbl, _p, _p, _p],
     "sfb_generate_uniform": [_i64, _i64, _u64, _dbl, _dbl, _p, _p],
+    "sfb_generate_modal_states": [_i64, _i64, _i64, _u64, _p, _p, _dbl, _p, _p],
+    "sfb_generate_metric": [_i64, _i64, _i64, _u64, _p, _i64, _dbl, _p, _p],
 }
 _RESTYPES = {
     "sfb_last_error": ctypes.c_char_p,

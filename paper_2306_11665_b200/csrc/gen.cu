@@ -60,6 +60,80 @@ __global__ void generate_euler_kernel(int64_t E, int64_t e0, int64_t nodes, uint
   }
 }
 
+// Modal coefficients (config 5): idx = (e*5 + v)*modes + k,
+// Uhat = (amp_v 2^-(k0+k1+k2)) (2u - 1)  (+ mean_v c0 at k = 0).
+struct ModalGenParams {
+  double mean[5], amp[5], c0;
+};
+
+__global__ void generate_modal_kernel(int64_t E, int64_t e0, int n, uint64_t key,
+                                      ModalGenParams prm, double* __restrict__ Uhat) {
+  const int64_t modes = (int64_t)n * n * n;
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t total = E * 5 * modes;
+  for (; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = t / (5 * modes);
+    const int64_t rem = t - e * 5 * modes;
+    const int v = (int)(rem / modes);
+    const int k = (int)(rem - (int64_t)v * modes);
+    const uint64_t idx = ((uint64_t)(e0 + e) * 5 + v) * (uint64_t)modes + k;
+    const double w = __dsub_rn(__dmul_rn(2.0, u01(key, idx)), 1.0);
+    const int deg = k % n + (k / n) % n + k / (n * n);
+    double x = __dmul_rn(__dmul_rn(prm.amp[v], ldexp(1.0, -deg)), w);
+    if (k == 0) x = __dadd_rn(__dmul_rn(prm.mean[v], prm.c0), x);
+    Uhat[t] = x;
+  }
+}
+
+// Warped-lattice metric cofactors (config 5); see synth.metric_cofactors.
+struct MetricGenParams {
+  double nodes[16];
+  double phi[9];
+  double h, amp;
+  int64_t K;
+};
+
+__global__ void generate_metric_kernel(int64_t E, int64_t e0, int n, MetricGenParams prm,
+                                       double* __restrict__ Ja) {
+  const int64_t nodes = (int64_t)n * n * n;
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t total = E * nodes;
+  const double two_pi = 6.283185307179586;
+  for (; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = t / nodes;
+    const int r = (int)(t - e * nodes);
+    const int64_t cell = (e0 + e) % (prm.K * prm.K * prm.K);
+    const int64_t c[3] = {cell % prm.K, (cell / prm.K) % prm.K, cell / (prm.K * prm.K)};
+    const int rr[3] = {r % n, (r / n) % n, r / (n * n)};
+    double X[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) X[k] = ((double)c[k] + (prm.nodes[rr[k]] + 1.0) * 0.5) * prm.h;
+    double G[3][3];
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      double sn[3], cs[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) sincos(two_pi * (X[k] + prm.phi[m * 3 + k]), &sn[k], &cs[k]);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double prod = cs[i] * sn[(i + 1) % 3] * sn[(i + 2) % 3];
+        G[m][i] = 0.5 * prm.h * ((m == i ? 1.0 : 0.0) + prm.amp * two_pi * prod);
+      }
+    }
+    double* out = Ja + e * 9 * nodes + r;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        const int a = m == 0 ? 1 : 0, b = m == 2 ? 1 : 2;
+        const int cc = i == 0 ? 1 : 0, d = i == 2 ? 1 : 2;
+        const double minor = G[a][cc] * G[b][d] - G[a][d] * G[b][cc];
+        out[(i * 3 + m) * nodes] = ((i + m) % 2 == 0) ? minor : -minor;
+      }
+    }
+  }
+}
+
 // Perfect binary tree within each block: level k adds entries 2i and 2i+1 of
 // level k-1.  The order is a property of the data, not of the launch.
 __global__ void block_sums_kernel(const double* __restrict__ x, int64_t block,
@@ -113,6 +187,44 @@ extern "C" int sfb_generate_euler_states(int64_t E, int64_t e0, int64_t n, uint6
       E, e0, nodes, splitmix64(seed), gamma - 1.0, b[0], b[1] - b[0], b[2], b[3] - b[2], b[4],
       b[5] - b[4], U);
   return check_launch("generate_euler_states");
+}
+
+extern "C" int sfb_generate_modal_states(int64_t E, int64_t e0, int64_t n, uint64_t seed,
+                                         const double* means5, const double* amps5, double c0,
+                                         double* Uhat, sfb_stream_t stream) {
+  SFB_CHECK_ARG(E >= 0 && e0 >= 0 && n >= 1 && n <= 16, "bad extents");
+  SFB_CHECK_ARG(means5 && amps5, "null means/amps (host arrays of 5)");
+  if (E == 0) return SFB_OK;
+  SFB_CHECK_ARG(Uhat != nullptr, "null output");
+  ModalGenParams prm;
+  for (int v = 0; v < 5; ++v) {
+    prm.mean[v] = means5[v];
+    prm.amp[v] = amps5[v];
+  }
+  prm.c0 = c0;
+  generate_modal_kernel<<<grid_cap(E * 5 * n * n * n), 256, 0, (cudaStream_t)stream>>>(
+      E, e0, (int)n, splitmix64(seed), prm, Uhat);
+  return check_launch("generate_modal_states");
+}
+
+extern "C" int sfb_generate_metric(int64_t E, int64_t e0, int64_t n, uint64_t seed,
+                                   const double* nodes, int64_t K, double amp, double* Ja,
+                                   sfb_stream_t stream) {
+  SFB_CHECK_ARG(E >= 0 && e0 >= 0 && n >= 1 && n <= 16 && K >= 1, "bad extents");
+  SFB_CHECK_ARG(nodes != nullptr, "null nodes (host array of n)");
+  if (E == 0) return SFB_OK;
+  SFB_CHECK_ARG(Ja != nullptr, "null output");
+  MetricGenParams prm;
+  for (int i = 0; i < n; ++i) prm.nodes[i] = nodes[i];
+  const uint64_t key = splitmix64(seed);
+  for (int i = 0; i < 9; ++i)
+    prm.phi[i] = (double)(splitmix64(key + (uint64_t)i) >> 11) * 0x1.0p-53;
+  prm.h = 1.0 / (double)K;
+  prm.amp = amp;
+  prm.K = K;
+  generate_metric_kernel<<<grid_cap(E * n * n * n), 256, 0, (cudaStream_t)stream>>>(
+      E, e0, (int)n, prm, Ja);
+  return check_launch("generate_metric");
 }
 
 extern "C" int sfb_block_sums(const double* x, int64_t count, int64_t block, double* partial,

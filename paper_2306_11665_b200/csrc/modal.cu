@@ -1,9 +1,422 @@
-// K4: curvilinear modal Euler volume term (config 5).  Placeholder until the
-// fused kernel lands; reports ENOTSUP so callers fail loudly.
+// K4: curvilinear, modal Euler volume term (BASELINE config 5).
+//
+//   u    = (V x V x V) Uhat                      modal -> GLL nodal (kronecker_apply,
+//                                                 operators.py:274-318)
+//   r    = scale sum_i sum_l D[r_i,l] Ft_i(u_r, u_r(i->l))
+//          Ft_i(a,b) = F#(a, b; n = (Ja^i(a) + Ja^i(b))/2)   contravariant flux
+//                                                 differencing (burgers.py:117-131
+//                                                 generalised; Hadamard + row sum)
+//   Rhat = (Pi x Pi x Pi) r                      nodal -> modal projection
+//   sumsq[e] = sum Rhat[e]^2                     (fixed-order partial of the norm)
+//
+// One persistent CTA processes one element per iteration; the next element's
+// Uhat and Ja (8.6 KB + 15.6 KB at n = 6) are prefetched with two 1-D bulk
+// copies (cp.async.bulk, UBLKCP) into the other half of a double buffer while
+// the current element is transformed, differenced and projected - all in
+// shared memory, so HBM sees exactly Uhat + Ja in and Rhat (+ 8 B) out.
+//   stage A  three sum-factorised passes of V (one per direction), thread per
+//            (variable, line), ping-ponging between the input slot and scratch;
+//   stage B  thread per node: primitives, per-node logs, node record; the
+//            diagonal term sum_i D[r_i,r_i] F#(u_r,u_r; Ja^i(r)) into the
+//            residual (consistency: F#(u,u;n) = f(u).n);
+//   stage C  thread per (direction, line): each symmetric pair once, scattered
+//            to both rows; direction-ordered accumulation (3 barrier phases);
+//   stage D  three passes of Pi; Rhat streamed out; per-thread squares summed
+//            in a fixed order, then a fixed smem tree -> sumsq[e].
+// The metric averaging 1/2 is folded into D (Ft is linear in n).
+#include "bulk.cuh"
 #include "common.cuh"
+#include "euler_flux.cuh"
 
-extern "C" int sfb_euler_volume_curvilinear_modal(int64_t, int64_t, const double*, const double*,
-                                                  const double*, double, double, const double*,
-                                                  const double*, double*, double*, sfb_stream_t) {
-  return sfb::fail(SFB_ENOTSUP, "euler_volume_curvilinear_modal: not built yet");
+namespace sfb {
+
+template <int N>
+struct ModalOps {
+  double D[N * N];   // scale * D / 2 (the 1/2 of the metric average folded in)
+  double V[N * N];   // Vandermonde (interpolation)
+  double P[N * N];   // projection
+  double Dd[N];      // scale * D[i][i] (diagonal term, full metric at the node)
+};
+
+template <int N>
+struct ModalCfg {
+  static constexpr int kNodes = N * N * N;
+  static constexpr int kLines = N * N;
+  static constexpr int kLineThreads = 3 * kLines;
+  static constexpr int kThreads = ((kLineThreads + 31) / 32) * 32 < 128 ? 128
+                                  : ((kLineThreads + 31) / 32) * 32;
+  static constexpr int kU = 5 * kNodes;   // doubles of Uhat / u / r per element
+  static constexpr int kJ = 9 * kNodes;   // doubles of Ja per element
+  static constexpr int kSlot = kU + kJ;   // one input slot
+  static constexpr int kRec = 9 * kNodes; // node records: 8 planes + p
+  static constexpr int kRedPow2 = kThreads <= 128 ? 128 : (kThreads <= 256 ? 256 : 512);
+  static constexpr size_t kSmem =
+      (size_t)(2 * kSlot + kU /*scratch*/ + kRec + kU /*residual*/ + kRedPow2) * sizeof(double);
+};
+
+// one sum-factorised pass along direction j: out[.., a_j, ..] = sum_c A[a_j][c] in[.., c, ..]
+template <int N>
+__device__ __forceinline__ void kron_pass(const double* __restrict__ A, int j,
+                                          const double* __restrict__ in, double* __restrict__ out,
+                                          int tid, int nthreads) {
+  constexpr int NN = N * N * N;
+  const int stride = j == 0 ? 1 : (j == 1 ? N : N * N);
+  for (int t = tid; t < 5 * N * N; t += nthreads) {
+    const int v = t / (N * N);
+    const int L = t - v * N * N;
+    const int u0 = L % N, u1 = L / N;
+    int base;
+    if (j == 0) base = u0 * N + u1 * N * N;
+    else if (j == 1) base = u0 + u1 * N * N;
+    else base = u0 + u1 * N;
+    const double* src = in + v * NN + base;
+    double x[N];
+#pragma unroll
+    for (int c = 0; c < N; ++c) x[c] = src[c * stride];
+    double* dst = out + v * NN + base;
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+      double acc = 0.0;
+#pragma unroll
+      for (int c = 0; c < N; ++c) acc = fma(A[a * N + c], x[c], acc);
+      dst[a * stride] = acc;
+    }
+  }
+}
+
+// Contravariant Chandrashekar flux for K pairs at once (normals n = Ja_a + Ja_b,
+// the 1/2 being folded into D).
+template <int K>
+__device__ __forceinline__ void chandrashekar_curv_k(const NodeRec (&A)[K],
+                                                     const NodeRec (&B)[K],
+                                                     const double (&nx)[K], const double (&ny)[K],
+                                                     const double (&nz)[K], double c_gamma,
+                                                     double (&f)[K][5]) {
+  double vb0[K], vb1[K], vb2[K], nr[K], dr[K], nb[K], db[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    vb0[k] = A[k].hv0 + B[k].hv0;
+    vb1[k] = A[k].hv1 + B[k].hv1;
+    vb2[k] = A[k].hv2 + B[k].hv2;
+    logmean_parts(A[k].hr, B[k].hr, A[k].hlr, B[k].hlr, nr[k], dr[k]);
+    logmean_parts(A[k].hb, B[k].hb, A[k].hlb, B[k].hlb, nb[k], db[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const double sr = A[k].hr + B[k].hr;
+    const double sb = A[k].hb + B[k].hb;
+    const double p1 = dr[k] * nb[k];
+    const double rr = rcp_refined(p1 * sb);
+    const double inv_sb = rr * p1;
+    const double t = rr * sb;
+    const double rho_ln = nr[k] * (t * nb[k]);
+    const double ibeta = db[k] * (t * dr[k]);
+    const double phat = 0.5 * sr * inv_sb;
+    const double vn = fma(vb2[k], nz[k], fma(vb1[k], ny[k], vb0[k] * nx[k]));
+    const double f1 = rho_ln * vn;
+    f[k][0] = f1;
+    f[k][1] = fma(f1, vb0[k], phat * nx[k]);
+    f[k][2] = fma(f1, vb1[k], phat * ny[k]);
+    f[k][3] = fma(f1, vb2[k], phat * nz[k]);
+    const double vv = fma(vb2[k], vb2[k], fma(vb1[k], vb1[k], vb0[k] * vb0[k]));
+    const double g = fma(c_gamma, ibeta, vv - (A[k].q + B[k].q));
+    f[k][4] = fma(f1, g, phat * vn);
+  }
+}
+
+template <int N>
+struct ModalPairs {
+  static constexpr int kPairs = N * (N - 1) / 2;
+  int a[kPairs > 0 ? kPairs : 1], b[kPairs > 0 ? kPairs : 1];
+  constexpr ModalPairs() : a{}, b{} {
+    const int M = (N % 2 == 0) ? N : N + 1;
+    int k = 0;
+    for (int round = 0; round < M - 1; ++round) {
+      for (int i = 0; i < M / 2; ++i) {
+        int x = (i == 0) ? M - 1 : (round + i) % (M - 1);
+        int y = (i == 0) ? round : (round - i + (M - 1)) % (M - 1);
+        if (x >= N || y >= N) continue;
+        a[k] = x < y ? x : y;
+        b[k] = x < y ? y : x;
+        ++k;
+      }
+    }
+  }
+};
+
+template <int N>
+constexpr int kModalBatch = (N >= 7) ? 1 : (N == 6 ? 3 : (N >= 4 ? 2 : 1));
+
+template <int N>
+__global__ void __launch_bounds__(ModalCfg<N>::kThreads)
+    euler_modal_kernel(int64_t E, const ModalOps<N> ops, double gm1, double c_gamma,
+                       double gam_ratio, const double* __restrict__ Uhat,
+                       const double* __restrict__ Ja, double* __restrict__ Rhat,
+                       double* __restrict__ sumsq) {
+  using Cfg = ModalCfg<N>;
+  constexpr int NN = Cfg::kNodes;
+  constexpr int T = Cfg::kThreads;
+  extern __shared__ __align__(16) double smem[];
+  double* slots = smem;                    // [2][Uhat | Ja]
+  double* scratch = smem + 2 * Cfg::kSlot; // [5][NN]
+  double* rec = scratch + Cfg::kU;         // [9][NN] node records (natural layout)
+  double* res = rec + Cfg::kRec;           // [5][NN] nodal residual r
+  double* red = res + Cfg::kU;             // [T] reduction scratch
+  __shared__ uint64_t full[2];
+  __shared__ double sops[3 * N * N + N];
+  const int tid = threadIdx.x;
+  if (tid == 0) {  // static indices only: the parameter block is never copied to local memory
+#pragma unroll
+    for (int i = 0; i < N * N; ++i) {
+      sops[i] = ops.D[i];
+      sops[N * N + i] = ops.V[i];
+      sops[2 * N * N + i] = ops.P[i];
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) sops[3 * N * N + i] = ops.Dd[i];
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const double* sD = sops;
+  const double* sV = sops + N * N;
+  const double* sP = sops + 2 * N * N;
+  const double* sDd = sops + 3 * N * N;
+
+  constexpr uint32_t kUB = (uint32_t)(Cfg::kU * 8), kJB = (uint32_t)(Cfg::kJ * 8);
+  constexpr bool kBulk = (kUB % 16) == 0 && (kJB % 16) == 0;
+  auto issue = [&](int64_t e, int slot) {
+    double* dst = slots + slot * Cfg::kSlot;
+    mbar_arrive_expect_tx(&full[slot], kUB + kJB);
+    bulk_g2s(dst, Uhat + e * Cfg::kU, kUB, &full[slot]);
+    bulk_g2s(dst + Cfg::kU, Ja + e * Cfg::kJ, kJB, &full[slot]);
+  };
+  if (kBulk && tid == 0 && (int64_t)blockIdx.x < E) issue(blockIdx.x, 0);
+  uint32_t parity[2] = {0, 0};
+
+  int it = 0;
+  for (int64_t e = blockIdx.x; e < E; e += gridDim.x, ++it) {
+    const int slot = it & 1;
+    double* in = slots + slot * Cfg::kSlot;
+    const double* jin = in + Cfg::kU;
+    if (kBulk) {
+      mbar_wait_parity(&full[slot], parity[slot]);
+      parity[slot] ^= 1;
+      const int64_t nxt = e + gridDim.x;
+      if (tid == 0 && nxt < E) {
+        fence_proxy_async_smem();
+        issue(nxt, slot ^ 1);
+      }
+    } else {
+      for (int i = tid; i < Cfg::kU; i += T) in[i] = __ldcs(Uhat + e * Cfg::kU + i);
+      for (int i = tid; i < Cfg::kJ; i += T) in[Cfg::kU + i] = __ldcs(Ja + e * Cfg::kJ + i);
+      __syncthreads();
+    }
+
+    // ---- stage A: u = V^3 Uhat ------------------------------------------------
+    kron_pass<N>(sV, 0, in, scratch, tid, T);
+    __syncthreads();
+    kron_pass<N>(sV, 1, scratch, in, tid, T);
+    __syncthreads();
+    kron_pass<N>(sV, 2, in, scratch, tid, T);  // u in scratch
+    __syncthreads();
+
+    // ---- stage B: node records + diagonal term ----------------------------------
+    for (int r = tid; r < NN; r += T) {
+      const double* u = scratch + r;
+      const double rho = u[0], m0 = u[NN], m1 = u[2 * NN], m2 = u[3 * NN], et = u[4 * NN];
+      const double irho = rcp_refined(rho);
+      const double v0 = m0 * irho, v1 = m1 * irho, v2 = m2 * irho;
+      const double vv = fma(v2, v2, fma(v1, v1, v0 * v0));
+      const double p = gm1 * fma(-0.5 * rho, vv, et);
+      const double beta = 0.5 * rho * rcp_refined(p);
+      rec[r] = 0.5 * rho;
+      rec[NN + r] = 0.5 * v0;
+      rec[2 * NN + r] = 0.5 * v1;
+      rec[3 * NN + r] = 0.5 * v2;
+      rec[4 * NN + r] = 0.5 * beta;
+      rec[5 * NN + r] = 0.5 * log_pos(rho);
+      rec[6 * NN + r] = 0.5 * log_pos(beta);
+      rec[7 * NN + r] = 0.25 * vv;
+      rec[8 * NN + r] = p;
+      // n_diag = sum_i D[r_i,r_i] Ja^i(r)
+      const int c0 = r % N, c1 = (r / N) % N, c2 = r / (N * N);
+      const double d0 = sDd[c0], d1 = sDd[c1], d2 = sDd[c2];
+      double nd[3];
+#pragma unroll
+      for (int m = 0; m < 3; ++m)
+        nd[m] = fma(d2, jin[(2 * 3 + m) * NN + r],
+                    fma(d1, jin[(1 * 3 + m) * NN + r], d0 * jin[(0 * 3 + m) * NN + r]));
+      const double vn = fma(v2, nd[2], fma(v1, nd[1], v0 * nd[0]));
+      res[r] = rho * vn;
+      res[NN + r] = fma(m0, vn, p * nd[0]);
+      res[2 * NN + r] = fma(m1, vn, p * nd[1]);
+      res[3 * NN + r] = fma(m2, vn, p * nd[2]);
+      res[4 * NN + r] = fma(gam_ratio * p, vn, 0.5 * rho * vv * vn);  // (E + p) vn
+      (void)et;
+    }
+    __syncthreads();
+
+    // ---- stage C: line threads --------------------------------------------------
+    {
+      const int dir = tid / Cfg::kLines;
+      const int L = tid - dir * Cfg::kLines;
+      const bool active = tid < Cfg::kLineThreads;
+      const int u0 = L % N, u1 = L / N;
+      int base, stride;
+      if (dir == 0) { base = u0 * N + u1 * N * N; stride = 1; }
+      else if (dir == 1) { base = u0 + u1 * N * N; stride = N; }
+      else { base = u0 + u1 * N; stride = N * N; }
+      double acc[N][5];
+#pragma unroll
+      for (int a = 0; a < N; ++a)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) acc[a][v] = 0.0;
+      if (active) {
+        constexpr ModalPairs<N> po;
+        constexpr int P = ModalPairs<N>::kPairs;
+        constexpr int K = kModalBatch<N>;
+        const double* jd = jin + (dir * 3) * NN;  // Ja^dir_m planes
+        auto load = [&](int a) {
+          NodeRec q;
+          const int k = base + a * stride;
+          q.hr = rec[k];
+          q.hv0 = rec[NN + k];
+          q.hv1 = rec[2 * NN + k];
+          q.hv2 = rec[3 * NN + k];
+          q.hb = rec[4 * NN + k];
+          q.hlr = rec[5 * NN + k];
+          q.hlb = rec[6 * NN + k];
+          q.q = rec[7 * NN + k];
+          return q;
+        };
+#pragma unroll
+        for (int k0 = 0; k0 < P; k0 += K) {
+          NodeRec A[K], B[K];
+          double nx[K], ny[K], nz[K];
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const int kk = (k0 + k < P) ? k0 + k : P - 1;
+            const int a = po.a[kk], b = po.b[kk];
+            A[k] = load(a);
+            B[k] = load(b);
+            const int ka = base + a * stride, kb = base + b * stride;
+            nx[k] = jd[ka] + jd[kb];
+            ny[k] = jd[NN + ka] + jd[NN + kb];
+            nz[k] = jd[2 * NN + ka] + jd[2 * NN + kb];
+          }
+          double f[K][5];
+          chandrashekar_curv_k<K>(A, B, nx, ny, nz, c_gamma, f);
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            if (k0 + k >= P) break;
+            const int a = po.a[k0 + k], b = po.b[k0 + k];
+            const double dab = sD[a * N + b], dba = sD[b * N + a];
+#pragma unroll
+            for (int v = 0; v < 5; ++v) {
+              acc[a][v] = fma(dab, f[k][v], acc[a][v]);
+              acc[b][v] = fma(dba, f[k][v], acc[b][v]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int phase = 0; phase < 3; ++phase) {
+        if (active && dir == phase) {
+#pragma unroll
+          for (int a = 0; a < N; ++a)
+#pragma unroll
+            for (int v = 0; v < 5; ++v) res[v * NN + base + a * stride] += acc[a][v];
+        }
+        __syncthreads();
+      }
+    }
+
+    // ---- stage D: Rhat = Pi^3 r, store, sum of squares -------------------------
+    kron_pass<N>(sP, 0, res, scratch, tid, T);
+    __syncthreads();
+    kron_pass<N>(sP, 1, scratch, res, tid, T);
+    __syncthreads();
+    kron_pass<N>(sP, 2, res, scratch, tid, T);  // Rhat in scratch
+    __syncthreads();
+    double* Rg = Rhat + e * Cfg::kU;
+    double ss = 0.0;
+    for (int i = tid; i < Cfg::kU; i += T) {
+      const double x = scratch[i];
+      __stcs(Rg + i, x);
+      ss = fma(x, x, ss);
+    }
+    if (sumsq) {  // fixed-shape tree over a power-of-two padded array
+      constexpr int RP = Cfg::kRedPow2;
+      red[tid] = ss;
+      for (int i = T + tid; i < RP; i += T) red[i] = 0.0;
+      __syncthreads();
+      for (int w = RP / 2; w >= 1; w /= 2) {
+        for (int i = tid; i < w; i += T) red[i] = red[i] + red[i + w];
+        __syncthreads();
+      }
+      if (tid == 0) sumsq[e] = red[0];
+    }
+    __syncthreads();
+  }
+}
+
+template <int N>
+static int launch_modal(int64_t E, const double* V, const double* Pi, const double* D,
+                        double gamma, double scale, const double* Uhat, const double* Ja,
+                        double* Rhat, double* sumsq, cudaStream_t s) {
+  using Cfg = ModalCfg<N>;
+  ModalOps<N> ops;
+  for (int i = 0; i < N * N; ++i) {
+    ops.D[i] = 0.5 * scale * D[i];
+    ops.V[i] = V[i];
+    ops.P[i] = Pi[i];
+  }
+  for (int i = 0; i < N; ++i) ops.Dd[i] = scale * D[i * N + i];
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    cudaFuncSetAttribute(euler_modal_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Cfg::kSmem);
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, euler_modal_kernel<N>, Cfg::kThreads,
+                                                  Cfg::kSmem);
+    per_sm = b > 0 ? b : 1;
+  }
+  int64_t grid = (int64_t)num_sms() * per_sm;
+  if (grid > E) grid = E;
+  const double gm1 = gamma - 1.0;
+  euler_modal_kernel<N><<<(unsigned)grid, Cfg::kThreads, Cfg::kSmem, s>>>(
+      E, ops, gm1, 1.0 / (2.0 * gm1), gamma / gm1, Uhat, Ja, Rhat, sumsq);
+  return check_launch("euler_volume_curvilinear_modal");
+}
+
+}  // namespace sfb
+
+using namespace sfb;
+
+// V, Pi, D are HOST pointers (n x n operators folded into the parameter block).
+extern "C" int sfb_euler_volume_curvilinear_modal(int64_t E, int64_t n, const double* V,
+                                                  const double* Pi, const double* D, double gamma,
+                                                  double scale, const double* Uhat,
+                                                  const double* Ja, double* Rhat, double* sumsq,
+                                                  sfb_stream_t stream) {
+  SFB_CHECK_ARG(E >= 0, "negative element count");
+  SFB_CHECK_ARG(V && Pi && D, "null operator (host n x n arrays)");
+  SFB_CHECK_ARG(gamma > 1.0, "gamma must exceed 1");
+  if (E == 0) return SFB_OK;
+  SFB_CHECK_ARG(Uhat && Ja && Rhat, "null state / metric / output pointer");
+  SFB_CHECK_ARG(((uintptr_t)Uhat | (uintptr_t)Ja | (uintptr_t)Rhat) % 16 == 0,
+                "Uhat, Ja, Rhat must be 16-byte aligned");
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (n) {
+    case 2: return launch_modal<2>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s);
+    case 3: return launch_modal<3>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s);
+    case 4: return launch_modal<4>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s);
+    case 5: return launch_modal<5>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s);
+    case 6: return launch_modal<6>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s);
+    case 7: return launch_modal<7>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s);
+    case 8: return launch_modal<8>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s);
+    default: return fail(SFB_ENOTSUP, "euler_volume_curvilinear_modal: n must be in 2..8");
+  }
 }

@@ -148,3 +148,24 @@ def volume_curvilinear_modal(Uhat, Ja, n, gamma=GAMMA, scale=2.0, out=None, sums
         _lib.ptr(sumsq), _lib.stream_ptr(stream),
     )
     return out
+
+
+def generate_modal_states(E, n, seed, e0=0, device=None):
+    """Device-side config-5 modal coefficients, bitwise equal to synth.modal_states."""
+    _lib.require_cuda()
+    U = torch.empty((E, 5, n**3), dtype=torch.float64, device=device or "cuda")
+    means = np.ascontiguousarray(synth.MODAL_MEANS, dtype=np.float64)
+    amps = np.ascontiguousarray(synth.MODAL_AMPS, dtype=np.float64)
+    _lib.call("sfb_generate_modal_states", E, e0, n, seed, means.ctypes.data, amps.ctypes.data,
+              float(synth.MODAL_C0), _lib.ptr(U), _lib.stream_ptr())
+    return U
+
+
+def generate_metric(E, n, seed, e0=0, K=synth.MESH_K, amp=synth.WARP_AMP, device=None):
+    """Device-side warped-lattice metric cofactors (synth.metric_cofactors to ~1e-15)."""
+    _lib.require_cuda()
+    Ja = torch.empty((E, 3, 3, n**3), dtype=torch.float64, device=device or "cuda")
+    nodes = np.ascontiguousarray(gll_operators(n)[0].nodes, dtype=np.float64)
+    _lib.call("sfb_generate_metric", E, e0, n, seed, nodes.ctypes.data, K, float(amp),
+              _lib.ptr(Ja), _lib.stream_ptr())
+    return Ja

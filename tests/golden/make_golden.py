@@ -21,6 +21,8 @@ regenerate the same inputs without the reference):
                        hadamard_row_sum (index-trick operand), n = 2..8
   burgers.npz          volume_residual / time_derivative for seeded states
   kron.npz             kronecker_apply on seeded factor sets
+  euler_modal.npz      config 5: V^3 -> contravariant Chandrashekar volume term
+                       -> Pi^3 through kronecker_apply + the index-trick route
 Only tests read these files; nothing on the GPU box reads /root/reference.
 """
 
@@ -235,6 +237,60 @@ def make_kron(sf):
     np.savez_compressed(os.path.join(HERE, "kron.npz"), **out)
 
 
+MODAL_SAMPLE = {6: 3, 4: 3, 3: 2}
+
+
+def reference_curvilinear_modal(sf, Uhat, Ja, n, gamma=1.4, scale=2.0):
+    """Config 5 through the reference's own machinery: kronecker_apply for the
+    modal <-> nodal transforms (operators.py:274-318) and the index-trick
+    Hadamard route for the contravariant flux (kernel.py:195-266)."""
+    rule = sf.gauss_lobatto_legendre(n)
+    D = sf.lagrange_diff_matrix(rule)
+    V = sf.legendre_vandermonde(rule)
+    Pi = sf.projection_operator(rule, V)
+    d = 3
+    pattern = sf.build_sparsity_pattern(n, n, d)
+    basis = sf.assemble_basis_factors(pattern, D, np.ones(n))
+    E = Uhat.shape[0]
+    Rhat = np.empty_like(Uhat)
+    for e in range(E):
+        u = np.stack([sf.kronecker_apply([V, V, V], Uhat[e, v]) for v in range(5)])
+        rho, vel, p, beta, vv = euler_oracle.primitives(u, gamma)
+        r = np.empty_like(u)
+        for var in range(5):
+
+            def g(ri, ci, var=var):
+                ri = ri.astype(np.int64)
+                ci = ci.astype(np.int64)
+                out = np.empty(ri.shape)
+                for j in range(d):
+                    a = (rho[ri[:, j]], [vm[ri[:, j]] for vm in vel], p[ri[:, j]],
+                         beta[ri[:, j]], vv[ri[:, j]])
+                    b = (rho[ci[:, j]], [vm[ci[:, j]] for vm in vel], p[ci[:, j]],
+                         beta[ci[:, j]], vv[ci[:, j]])
+                    normal = [0.5 * (Ja[e, j, m][ri[:, j]] + Ja[e, j, m][ci[:, j]])
+                              for m in range(3)]
+                    out[:, j] = euler_oracle.chandrashekar(a, b, normal, gamma)[var]
+                return out
+
+            operand = sf.TwoPointOperand(np.arange(n**d, dtype=float), func=g)
+            product = sf.hadamard_evaluate(basis, sf.assemble_operand_factors(pattern, operand))
+            r[var] = scale * sf.hadamard_row_sum(product, pattern).sum(axis=0)
+        Rhat[e] = np.stack([sf.kronecker_apply([Pi, Pi, Pi], r[v]) for v in range(5)])
+    return Rhat
+
+
+def make_modal(sf):
+    out = {}
+    for n, E in MODAL_SAMPLE.items():
+        Uhat = synth.modal_states(E, n, seed=50 + n)
+        Ja = synth.metric_cofactors(E, n, seed=60 + n, e0=12345)
+        out[f"Uhat{n}"] = Uhat
+        out[f"Ja{n}"] = Ja
+        out[f"Rhat{n}"] = reference_curvilinear_modal(sf, Uhat, Ja, n)
+    np.savez_compressed(os.path.join(HERE, "euler_modal.npz"), **out)
+
+
 def main():
     sf = import_reference()
     make_operators(sf)
@@ -244,6 +300,7 @@ def main():
     make_euler(sf)
     make_burgers(sf)
     make_kron(sf)
+    make_modal(sf)
     print("golden fixtures written to", HERE)
 
 

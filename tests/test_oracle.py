@@ -241,3 +241,32 @@ def test_reference_pattern_formulas_d3():
                     assert tuple(cols[t]) == (i * n * n + j * n + l, i * n * n + l * n + k,
                                               l * n * n + j * n + k)
                     t += 1
+
+
+@pytest.mark.parametrize("n", [3, 4, 6])
+def test_modal_oracle_matches_reference_route(n):
+    # config 5 through the reference's kronecker_apply + Hadamard pipeline;
+    # BLAS vs einsum summation order in the transforms, amplified by the
+    # cancellation of a smooth residual (~100x), gives ~1e-14
+    g = golden("euler_modal.npz")
+    rule = op.gauss_lobatto_legendre(n)
+    D = op.lagrange_diff_matrix(rule)
+    V = op.legendre_vandermonde(rule)
+    Pi = op.projection_operator(rule, V)
+    R, ss = eo.euler_volume_curvilinear_modal(g[f"Uhat{n}"], g[f"Ja{n}"], V, Pi, D)
+    assert max_rel(R, g[f"Rhat{n}"]) <= 1e-13
+
+
+def test_modal_states_are_physical():
+    n = 6
+    Uh = synth.modal_states(64, n, seed=1)
+    V = op.legendre_vandermonde(op.gauss_lobatto_legendre(n))
+    u = eo.kron3(V, Uh)
+    rho, v, p, beta, vv = eo.primitives(u, 1.4)
+    assert rho.min() > 0.8 and rho.max() < 1.2 and p.min() > 0.85
+    Ja = synth.metric_cofactors(8, n, seed=2)
+    h = 1.0 / synth.MESH_K
+    # unwarped limit: Ja = (h/2)^2 I
+    J0 = synth.metric_cofactors(2, n, seed=2, amp=0.0)
+    assert np.allclose(J0[:, 0, 0], h * h / 4) and np.allclose(J0[:, 0, 1], 0.0)
+    assert np.all(np.isfinite(Ja))
