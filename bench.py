@@ -10,7 +10,12 @@ elements (distinct global element ids; weak scaling, no data-path
 collective; timing is the max over ranks).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config 3|2|4|5] [--n N]
+                    [--config 3|2|4|5]
+
+  --config 2   generic batched Hadamard + row sum + direction sum (n=4, 262,144 el.)
+  --config 4   config 3 swept over n = 2..8 with ~2^24 nodes each (one line, "sweep")
+  --config 5   curvilinear modal Euler, n = 6, 2^21 elements sharded over the
+               ranks (strong scaling) + the deterministic NCCL residual norm
 
 Rank 0 prints ONE JSON line.  Keys beyond the driver contract:
   element_dof_per_s     nodes / s (x5 for conserved DOF / s)
@@ -37,11 +42,13 @@ sys.path.insert(0, ROOT)
 
 HBM_FALLBACK_GBS = 6650.0
 DFMA_MEASURED_TFLOPS = 34.154  # tools/peaks/fp64_peak.cu on this pool's B200 (profiles/)
+METRIC = "FP64 Hadamard entries/s (3D Euler Chandrashekar flux differencing)"
 
-# Algorithmic work per element for the Chandrashekar volume term (DESIGN.md
-# "Algorithmic bytes and flops"): unique off-diagonal pairs x (43 flux + 20
-# accumulate) + diagonal entries x 18 + nodes x 16; bytes = 2 x 5 x n^3 x 8.
+# Algorithmic work per element:
+# unique off-diagonal pairs x (43 flux + 20 accumulate) + diagonal entries x 18
+# + nodes x 16 (Cartesian); bytes = 2 x 5 x n^3 x 8.
 FLUX_FLOPS, ACC_FLOPS, DIAG_FLOPS, NODE_FLOPS = 43, 20, 18, 16
+CURV_EXTRA_FLOPS = 9  # contravariant: metric average (3 add) + v.n (3) + p n (3)
 
 
 def euler_flops_per_element(n):
@@ -51,6 +58,17 @@ def euler_flops_per_element(n):
 
 def euler_bytes_per_element(n):
     return 2 * 5 * n**3 * 8
+
+
+def modal_flops_per_element(n):
+    pairs = 3 * n * n * n * (n - 1) // 2
+    transforms = 2 * 2 * 5 * 3 * n ** 4  # V^3 and Pi^3, FMA = 2
+    return (transforms + pairs * (FLUX_FLOPS + CURV_EXTRA_FLOPS + ACC_FLOPS)
+            + 3 * n**3 * DIAG_FLOPS + n**3 * NODE_FLOPS + 2 * 5 * n**3)
+
+
+def modal_bytes_per_element(n):
+    return (5 + 9 + 5) * n**3 * 8 + 8
 
 
 def measured_peaks():
@@ -133,6 +151,32 @@ def cpu_model():
     return "unknown"
 
 
+def workload_config(args, world):
+    if args.config == 2:
+        return {"workload": f"config2: batched generic Hadamard + row sum + direction sum, "
+                            f"(D x I x I + I x D x I + I x I x D) o F, GLL n=4, {args.elements} "
+                            f"elements per GPU",
+                "n": 4, "elements_per_gpu": args.elements, "total_elements": args.elements * world,
+                "l2": "inputs (%.0f MB) larger than the 126 MB L2" % (args.elements * 6144 / 1e6),
+                "parallelism": f"element shards x{world}"}
+    if args.config == 5:
+        return {"workload": f"config5: curvilinear modal Euler (V^3 -> contravariant "
+                            f"Chandrashekar flux differencing -> Pi^3), GLL n={args.n}, "
+                            f"{args.elements} elements total, sharded, deterministic NCCL "
+                            f"residual norm",
+                "n": args.n, "total_elements": args.elements,
+                "elements_per_gpu": args.elements // world, "gamma": 1.4, "vars": 5,
+                "l2": "inputs (%.1f GB) larger than the 126 MB L2"
+                      % (args.elements * modal_bytes_per_element(args.n) / 1e9),
+                "parallelism": f"element shards x{world} (strong scaling)"}
+    return {"workload": f"config3: 3-D Euler Chandrashekar volume term, GLL n={args.n} "
+                        f"(p={args.n - 1}), {args.elements} Cartesian elements per GPU",
+            "n": args.n, "elements_per_gpu": args.elements, "total_elements": args.elements * world,
+            "gamma": 1.4, "vars": 5, "layout": "U[E][5][n^3] fp64 SoA",
+            "l2": "inputs (%.0f MB) larger than the 126 MB L2" % (args.elements * 5 * args.n**3 * 8 / 1e6),
+            "parallelism": f"element shards x{world}"}
+
+
 # ---------------------------------------------------------------------------
 # reference arm: the oracle's C port on the host cores (rank 0 only)
 # ---------------------------------------------------------------------------
@@ -144,32 +188,43 @@ def run_reference(args):
     from paper_2306_11665_b200 import synth
     from paper_2306_11665_b200.operators import gauss_lobatto_legendre, lagrange_diff_matrix
 
-    n, E = args.n, args.elements
     threads = os.cpu_count() or 1
-    D = lagrange_diff_matrix(gauss_lobatto_legendre(n))
-    U = synth.euler_states(E, n, seed=3)
+    if args.config == 2:
+        n, E = 4, args.elements
+        D = lagrange_diff_matrix(gauss_lobatto_legendre(n))
+        # B_j[R,l] = D[r_j, l] (weights ones), as assemble_basis builds it
+        r = np.arange(n**3)
+        basis = np.stack([D[(r // n**j) % n] for j in range(3)])
+        F = synth.uniform_array(E * 768, 2, -1.0, 1.0).reshape(E, 3, 64, 4)
+        run = lambda: c_oracle.hadamard_rowsum_batched(basis, F, threads=threads)  # noqa: E731
+        units = E * 768
+        sample = f"full workload ({E} elements) per step"
+    else:
+        n, E = args.n, args.elements
+        D = lagrange_diff_matrix(gauss_lobatto_legendre(n))
+        U = synth.euler_states(E, n, seed=3)
+        run = lambda: c_oracle.euler_volume_cartesian(U, D, threads=threads)  # noqa: E731
+        units = E * 3 * n**4
+        sample = f"full workload ({E} elements) per step"
     for _ in range(args.warmup):
-        c_oracle.euler_volume_cartesian(U, D, threads=threads)
+        run()
     times = []
     for _ in range(args.steps):
         t = time.perf_counter()
-        c_oracle.euler_volume_cartesian(U, D, threads=threads)
+        run()
         times.append(time.perf_counter() - t)
     sec = sum(times) / len(times)
-    entries = E * 3 * n ** 4
-    value = entries / sec
+    value = units / sec
     line = {
-        "metric": "FP64 Hadamard entries/s (3D Euler Chandrashekar flux differencing)",
+        "metric": METRIC if args.config != 2 else "FP64 Hadamard entries/s (generic batched)",
         "impl": "reference",
         "value": value, "unit": "entries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args, world),
-        "element_dof_per_s": E * n**3 / sec,
         "cpu_baseline": {"value": value, "unit": "entries/s", "cores": threads, "kind": "port",
-                         "sample": f"full workload ({E} elements) per step, C port of the "
-                                   f"oracle (oracle/euler_oracle.c), {threads} threads on "
-                                   f"{cpu_model()}"},
+                         "sample": f"{sample}, C port of the oracle (oracle/euler_oracle.c), "
+                                   f"{threads} threads on {cpu_model()}"},
         "e2e": {"value": value, "unit": "entries/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -177,42 +232,16 @@ def run_reference(args):
     return 0
 
 
-def workload_config(args, world):
-    return {"workload": f"config3: 3-D Euler Chandrashekar volume term, GLL n={args.n} "
-                        f"(p={args.n - 1}), {args.elements} Cartesian elements per GPU",
-            "n": args.n, "elements_per_gpu": args.elements, "total_elements": args.elements * world,
-            "gamma": 1.4, "vars": 5, "layout": "U[E][5][n^3] fp64 SoA",
-            "l2": "inputs (%.0f MB) larger than the 126 MB L2" % (args.elements * 5 * args.n**3 * 8 / 1e6),
-            "parallelism": f"element shards x{world}"}
-
-
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
-def run_ours(args):
+def timed_loop(step, steps, warmup, world, dist, stream, sampler):
+    """W untimed steps, then K steps between barrier+sync pairs; per-step events."""
     import torch
-    import torch.distributed as dist
 
     from paper_2306_11665_b200 import _lib
-    from paper_2306_11665_b200 import euler as eu
 
-    world, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-    n, E = args.n, args.elements
-    U = eu.generate_states(E, n, seed=3, e0=rank * E, device=dev)
-    R = torch.empty_like(U)
-    stream = torch.cuda.current_stream()
-
-    def step():
-        eu.volume_cartesian(U, n, out=R)
-
-    sampler = ClockSampler(local)
-    sampler.start()
-    time.sleep(0.3)
-    for _ in range(max(args.warmup, 3)):
+    for _ in range(max(warmup, 3)):
         step()
     torch.cuda.synchronize()
     if world > 1:
@@ -220,7 +249,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     launches0 = _lib.launch_count()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
+          for _ in range(steps)]
     t0 = time.time()
     for a, b in ev:
         a.record(stream)
@@ -234,55 +263,207 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    sampler.stop()
-    clocks = sampler.summary(t0, t1)
+    return ms_total / steps, per, launches, (t0, t1)
 
-    ms_step = ms_total / args.steps
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2306_11665_b200 import euler as eu
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
     if world > 1:
-        t = torch.tensor([ms_step], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_step = float(t.item())
-    kernel_ms = float(np.mean(per))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
 
-    entries = world * E * 3 * n**4
-    value = entries / (ms_step / 1e3)
-    hbm_gbs, peak_kind = measured_peaks()
-    bytes_launch = euler_bytes_per_element(n) * E
-    flops_launch = euler_flops_per_element(n) * E
-    achieved = bytes_launch / (kernel_ms / 1e3) / 1e9
-    achieved_tf = flops_launch / (kernel_ms / 1e3) / 1e12
+    if args.config == 4:
+        line = run_sweep(args, world, rank, dev, stream, sampler, dist)
+    elif args.config == 5:
+        line = run_modal(args, world, rank, dev, stream, sampler, dist)
+    elif args.config == 2:
+        line = run_hadamard(args, world, rank, dev, stream, sampler, dist)
+    else:
+        n, E = args.n, args.elements
+        U = eu.generate_states(E, n, seed=3, e0=rank * E, device=dev)
+        R = torch.empty_like(U)
 
-    line = {
-        "metric": "FP64 Hadamard entries/s (3D Euler Chandrashekar flux differencing)",
-        "value": value, "unit": "entries/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded counter-hash states, device-generated)",
-        "config": workload_config(args, world),
-        "element_dof_per_s": world * E * n**3 / (ms_step / 1e3),
-        "gpu_launches": launches,
-        "clocks": clocks,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_gbs, "unit": "GB/s",
-                     "frac": achieved / hbm_gbs, "traffic": args.traffic,
-                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                     "algorithmic_bytes_per_element": euler_bytes_per_element(n),
-                     "kernel_ms": kernel_ms},
-        "roofline_fp64": {"achieved": achieved_tf, "peak": DFMA_MEASURED_TFLOPS,
-                          "unit": "TFLOP/s", "frac": achieved_tf / DFMA_MEASURED_TFLOPS,
-                          "algorithmic_flops_per_element": euler_flops_per_element(n),
-                          "peak_source": "tools/peaks/fp64_peak.cu DFMA burst (profiles/fp64_peak.json)"},
-    }
+        def step():
+            eu.volume_cartesian(U, n, out=R)
 
-    if rank == 0 and world == 1 and not args.no_e2e:
-        line["e2e"] = measure_e2e(args, U)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = measure_cpu_baseline(args, U)
+        ms_step, per, launches, (t0, t1) = timed_loop(step, args.steps, args.warmup, world, dist,
+                                                      stream, sampler)
+        line = finish_line(args, world, dev, dist, ms_step, per, launches, sampler, t0, t1,
+                           units=E * 3 * n**4, unit="entries/s",
+                           bytes_launch=euler_bytes_per_element(n) * E,
+                           flops_launch=euler_flops_per_element(n) * E,
+                           extra={"element_dof_per_s": None, "dof_per_element": n**3})
+        line["element_dof_per_s"] = world * E * n**3 / (line["ms_per_step"] / 1e3)
+        if rank == 0 and world == 1 and not args.no_e2e:
+            line["e2e"] = measure_e2e(args, U)
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = measure_cpu_baseline(args, U)
+    sampler.stop()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def finish_line(args, world, dev, dist, ms_step, per, launches, sampler, t0, t1, units, unit,
+                bytes_launch, flops_launch, extra=None, metric=METRIC):
+    import torch
+
+    if world > 1:
+        t = torch.tensor([ms_step], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    kernel_ms = float(np.mean(per))
+    hbm_gbs, peak_kind = measured_peaks()
+    achieved = bytes_launch / (kernel_ms / 1e3) / 1e9
+    achieved_tf = flops_launch / (kernel_ms / 1e3) / 1e12
+    line = {
+        "metric": metric,
+        "value": world * units / (ms_step / 1e3), "unit": unit, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "strong" if args.config == 5 else "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded counter-hash inputs, device-generated)",
+        "config": workload_config(args, world),
+        "gpu_launches": launches,
+        "clocks": sampler.summary(t0, t1),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_gbs, "unit": "GB/s",
+                     "frac": achieved / hbm_gbs, "traffic": args.traffic,
+                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                     "algorithmic_bytes_per_launch": bytes_launch, "kernel_ms": kernel_ms},
+        "roofline_fp64": {"achieved": achieved_tf, "peak": DFMA_MEASURED_TFLOPS,
+                          "unit": "TFLOP/s", "frac": achieved_tf / DFMA_MEASURED_TFLOPS,
+                          "algorithmic_flops_per_launch": flops_launch,
+                          "peak_source": "tools/peaks/fp64_peak.cu DFMA burst (profiles/fp64_peak.json)"},
+    }
+    if args.config == 5 or flops_launch / bytes_launch > DFMA_MEASURED_TFLOPS * 1e3 / hbm_gbs:
+        # compute-bound by the algorithmic count: the FP64 roofline is the binding one
+        line["roofline"], line["roofline_hbm"] = dict(line["roofline_fp64"], bound="fp64",
+                                                      traffic=args.traffic,
+                                                      kernel_ms=kernel_ms), line["roofline"]
+        del line["roofline_fp64"]
+    if extra:
+        line.update({k: v for k, v in extra.items() if v is not None})
+    return line
+
+
+def run_hadamard(args, world, rank, dev, stream, sampler, dist):
+    import torch
+
+    import paper_2306_11665_b200 as sf
+    from paper_2306_11665_b200 import _lib
+    from paper_2306_11665_b200 import euler as eu
+
+    n, d, E = 4, 3, args.elements
+    D = sf.lagrange_diff_matrix(sf.gauss_lobatto_legendre(n))
+    pattern = sf.build_sparsity_pattern(n, n, d)
+    basis = sf.assemble_basis_factors(pattern, D, np.ones(n)).device
+    F = eu.generate_uniform(E * 768, 2, -1.0, 1.0, i0=rank * E * 768, device=dev)
+    out = torch.empty((E, 64), dtype=torch.float64, device=dev)
+
+    def step():
+        _lib.call("sfb_hadamard_rowsum_batched", E, n, n, d, _lib.ptr(basis), _lib.ptr(F), None,
+                  _lib.ptr(out), _lib.stream_ptr())
+
+    ms_step, per, launches, (t0, t1) = timed_loop(step, args.steps, args.warmup, world, dist,
+                                                  stream, sampler)
+    return finish_line(args, world, dev, dist, ms_step, per, launches, sampler, t0, t1,
+                       units=E * 768, unit="entries/s", bytes_launch=8 * (768 + 64) * E,
+                       flops_launch=2 * 768 * E, metric="FP64 Hadamard entries/s (generic batched)")
+
+
+def run_sweep(args, world, rank, dev, stream, sampler, dist):
+    import torch
+
+    from paper_2306_11665_b200 import euler as eu
+
+    points = []
+    t_first = None
+    for n in range(2, 9):
+        E = int(round(2**24 / n**3))
+        U = eu.generate_states(E, n, seed=4, e0=rank * E, device=dev)
+        R = torch.empty_like(U)
+
+        def step():
+            eu.volume_cartesian(U, n, out=R)
+
+        ms_step, per, launches, (t0, t1) = timed_loop(step, args.steps, args.warmup, world, dist,
+                                                      stream, sampler)
+        t_first = t_first or t0
+        kernel_ms = float(np.mean(per))
+        dof = E * n**3
+        points.append({"n": n, "p": n - 1, "elements": E, "ms_per_step": ms_step,
+                       "ns_per_dof": ms_step * 1e6 / dof,
+                       "entries_per_s": world * E * 3 * n**4 / (ms_step / 1e3),
+                       "hbm_frac": euler_bytes_per_element(n) * E / (kernel_ms / 1e3) / 1e9
+                       / measured_peaks()[0],
+                       "fp64_frac": euler_flops_per_element(n) * E / (kernel_ms / 1e3) / 1e12
+                       / DFMA_MEASURED_TFLOPS})
+        del U, R
+        torch.cuda.empty_cache()
+    # O(n^{d+1}) per element  <=>  time per DOF ~ n  (slope 1 in log-log)
+    ns = np.array([p["n"] for p in points], dtype=float)
+    t = np.array([p["ns_per_dof"] for p in points])
+    slope_all = float(np.polyfit(np.log(ns), np.log(t), 1)[0])
+    slope_cb = float(np.polyfit(np.log(ns[3:]), np.log(t[3:]), 1)[0])
+    best = min(points, key=lambda p: p["ms_per_step"])
+    line = finish_line(args, world, dev, dist, points[2]["ms_per_step"], [points[2]["ms_per_step"]],
+                       launches, sampler, t_first, time.time(),
+                       units=points[2]["elements"] * 3 * 4**4, unit="entries/s",
+                       bytes_launch=euler_bytes_per_element(4) * points[2]["elements"],
+                       flops_launch=euler_flops_per_element(4) * points[2]["elements"])
+    line["config"] = {"workload": "config4: config-3 kernel swept over n = 2..8, ~2^24 nodes each",
+                      "points": len(points)}
+    line["sweep"] = points
+    line["slope_time_per_dof_vs_n"] = {"all_n": slope_all, "n5_to_8": slope_cb,
+                                       "expected": "1 (O(n^{d+1}) per element / n^d DOF)"}
+    del best
+    return line
+
+
+def run_modal(args, world, rank, dev, stream, sampler, dist):
+    import torch
+
+    from paper_2306_11665_b200 import euler as eu
+    from paper_2306_11665_b200 import shard
+
+    n = args.n
+    total = args.elements
+    e0, E = shard.shard_range(total, rank, world)
+    Uh = eu.generate_modal_states(E, n, seed=5, e0=e0, device=dev)
+    Ja = eu.generate_metric(E, n, seed=6, e0=e0, device=dev)
+    Rh = torch.empty_like(Uh)
+    ss = torch.empty(E, dtype=torch.float64, device=dev)
+    block = 4096 if E % 4096 == 0 else 1
+    norm = [0.0]
+
+    def step():
+        eu.volume_curvilinear_modal(Uh, Ja, n, out=Rh, sumsq=ss)
+        norm[0] = shard.global_norm(ss, block=block)
+
+    ms_step, per, launches, (t0, t1) = timed_loop(step, args.steps, args.warmup, world, dist,
+                                                  stream, sampler)
+    line = finish_line(args, world, dev, dist, ms_step, per, launches, sampler, t0, t1,
+                       units=E * n**3, unit="element-DOF/s",
+                       bytes_launch=modal_bytes_per_element(n) * E,
+                       flops_launch=modal_flops_per_element(n) * E,
+                       metric="FP64 element-DOF/s (3D curvilinear modal Euler flux differencing)")
+    line["value"] = total * n**3 / (line["ms_per_step"] / 1e3)  # strong scaling: total DOF
+    line["residual_norm"] = norm[0]
+    line["hadamard_entries_per_s"] = total * 3 * n**4 / (line["ms_per_step"] / 1e3)
+    return line
 
 
 def measure_e2e(args, U_dev):
@@ -344,15 +525,26 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=4)
-    ap.add_argument("--elements", type=int, default=262144)
+    ap.add_argument("--config", type=int, default=3, choices=[2, 3, 4, 5])
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--elements", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=262144)
     ap.add_argument("--cpu-seconds", type=float, default=3.0)
     ap.add_argument("--traffic", type=float, default=None,
-                    help="ncu dram bytes per launch of the top kernel (from profiles/)")
+                    help="ncu dram bytes per launch of the top kernel (default: profiles/)")
     args = ap.parse_args(argv)
+    if args.traffic is None:
+        try:  # ncu --set full capture of the same kernel/config, summarised per round
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                args.traffic = json.load(f).get(f"config{args.config}")
+        except Exception:
+            args.traffic = None
+    if args.n is None:
+        args.n = 6 if args.config == 5 else 4
+    if args.elements is None:
+        args.elements = 2**21 if args.config == 5 else 262144
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
