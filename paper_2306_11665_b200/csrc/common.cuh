@@ -44,6 +44,17 @@ __device__ __forceinline__ double rcp_refined(double x) {
   return fma(r, e2, r);
 }
 
+// Guaranteed branch-free select (PTX selp).  A C++ ternary on doubles may be
+// lowered to a branch, which splits the basic block and stops ptxas from
+// interleaving independent work around it.
+__device__ __forceinline__ double dsel(bool p, double a, double b) {
+  double r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\tselp.f64 %0, %1, %2, q;\n\t}"
+      : "=d"(r)
+      : "d"(a), "d"(b), "r"((int)p));
+  return r;
+}
+
 // Stream-lined load of read-once data: bypass L1 allocation.
 __device__ __forceinline__ double2 ld_stream_d2(const double* p) {
   double2 v;

@@ -39,6 +39,12 @@
 #ifndef SFB_MINBLOCKS_N4
 #define SFB_MINBLOCKS_N4 4
 #endif
+#ifndef SFB_RECS_IN_REGS
+#define SFB_RECS_IN_REGS 0
+#endif
+#ifndef SFB_PREP_WARPS_N4
+#define SFB_PREP_WARPS_N4 1
+#endif
 
 namespace sfb {
 
@@ -57,7 +63,7 @@ struct EulerCartCfg {
   static constexpr int kLineThreads = 3 * kLines * kEPB;
   static constexpr int kLineWarps = (kLineThreads + 31) / 32;
   // prep warps balance node preprocessing + stores against the line work
-  static constexpr int kPrepWarps = (N <= 3) ? 3 : 1;
+  static constexpr int kPrepWarps = (N <= 3) ? 3 : (N == 4 ? SFB_PREP_WARPS_N4 : 1);
   static constexpr int kThreads = 32 * (kLineWarps + kPrepWarps);
   static constexpr int kMinBlocks = (N == 4) ? SFB_MINBLOCKS_N4 : 1;
   static constexpr int kVals = kEPB * 5 * kNodes;  // doubles per block of states
@@ -119,12 +125,12 @@ __device__ __forceinline__ void chandrashekar_cart_k(const NodeRec* const (&A)[K
     const double rho_ln = nr[k] * (t * nb[k]);
     const double ibeta = db[k] * (t * dr[k]);
     const double phat = 0.5 * sr[k] * inv_sb;
-    const double vn = dir == 0 ? vb0[k] : (dir == 1 ? vb1[k] : vb2[k]);
+    const double vn = dsel(dir == 0, vb0[k], dsel(dir == 1, vb1[k], vb2[k]));
     const double f1 = rho_ln * vn;
     f[k][0] = f1;
-    f[k][1] = fma(f1, vb0[k], dir == 0 ? phat : 0.0);
-    f[k][2] = fma(f1, vb1[k], dir == 1 ? phat : 0.0);
-    f[k][3] = fma(f1, vb2[k], dir == 2 ? phat : 0.0);
+    f[k][1] = fma(f1, vb0[k], dsel(dir == 0, phat, 0.0));
+    f[k][2] = fma(f1, vb1[k], dsel(dir == 1, phat, 0.0));
+    f[k][3] = fma(f1, vb2[k], dsel(dir == 2, phat, 0.0));
     const double vv = fma(vb2[k], vb2[k], fma(vb1[k], vb1[k], vb0[k] * vb0[k]));
     const double g = fma(c_gamma, ibeta, vv - (A[k]->q + B[k]->q));
     f[k][4] = fma(f1, g, phat * vn);
@@ -200,18 +206,30 @@ __device__ __forceinline__ void line_work(const double* __restrict__ rec, int el
   constexpr PairOrder<N> po;
   constexpr int P = PairOrder<N>::kPairs;
   constexpr int K = kPairBatch<N>;
+#if SFB_RECS_IN_REGS
   NodeRec nrec[N];
 #pragma unroll
   for (int a = 0; a < N; ++a) nrec[a] = load(a);
+#endif
 #pragma unroll
   for (int k0 = 0; k0 < P; k0 += K) {
     const NodeRec* A[K];
     const NodeRec* B[K];
+#if !SFB_RECS_IN_REGS
+    NodeRec ra[K], rb[K];  // records loaded per pair batch (fewer live registers)
+#endif
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const int kk = (k0 + k < P) ? k0 + k : P - 1;
+#if SFB_RECS_IN_REGS
       A[k] = &nrec[po.a[kk]];
       B[k] = &nrec[po.b[kk]];
+#else
+      ra[k] = load(po.a[kk]);
+      rb[k] = load(po.b[kk]);
+      A[k] = &ra[k];
+      B[k] = &rb[k];
+#endif
     }
     double f[K][5];
     chandrashekar_cart_k<K>(A, B, dir, c_gamma, f);
@@ -349,7 +367,7 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
     };
     int64_t blk = blockIdx.x;
     if (pt == 0 && niter > 0 && bulk_ok(blk)) issue(blk, 0);
-    uint32_t parity[2] = {0, 0};
+    uint32_t parity_bits = 0;  // bit k = phase of input slot k (no local-memory array)
     for (int it = 0; it < niter; ++it, blk += gridDim.x) {
       const int slot = it & 1;
       const int s = it & 1;
@@ -364,8 +382,8 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
         issue(nxt, slot ^ 1);
       }
       if (bulk_ok(blk)) {
-        mbar_wait_parity(&full[slot], parity[slot]);
-        parity[slot] ^= 1;
+        mbar_wait_parity(&full[slot], (parity_bits >> slot) & 1u);
+        parity_bits ^= 1u << slot;
       } else {  // odd-sized tail: plain loads
         for (int i = pt; i < nel * 5 * NN; i += kPrepT) in[i] = __ldcs(U + e0 * 5 * NN + i);
         nbar_sync(PREP_ONLY, kPrepT);

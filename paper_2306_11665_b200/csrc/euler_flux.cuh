@@ -33,10 +33,11 @@ __constant__ double kLogPoly[11] = {
 // Natural log for the per-node logarithms: x = 2^e m, m in [sqrt(1/2), sqrt(2)),
 // ln m = 2 atanh(f), f = (m-1)/(m+1), |f| <= 0.1716, degree-19 odd series
 // (truncation < 2.5e-17 relative).  ~22 FP64 operations, within ~2 ulp of the
-// correctly rounded value; non-positive / non-finite / subnormal inputs fall
-// back to libdevice log (keeps its NaN/inf semantics for invalid states).
+// correctly rounded value.  Branch-free (a branch would split the caller's
+// basic block and stop ptxas from interleaving independent nodes): inputs that
+// are not positive normal finite numbers - non-physical states - return NaN.
 __device__ __forceinline__ double log_pos(double x) {
-  if (!(x >= 2.2250738585072014e-308 && x <= 1.7976931348623157e308)) return log(x);
+  const bool ok = x >= 2.2250738585072014e-308 && x <= 1.7976931348623157e308;
   const int hi = __double2hiint(x), lo = __double2loint(x);
   int e = (hi >> 20) - 1023;
   int mh = (hi & 0x000fffff) | 0x3ff00000;
@@ -55,7 +56,8 @@ __device__ __forceinline__ double log_pos(double x) {
   for (int k = 7; k >= 0; --k) p = fma(p, f2, kLogPoly[k]);
   const double lnm = fma(f * f2, p, f + f);
   const double de = (double)e;
-  return fma(de, kLogPoly[9], fma(de, kLogPoly[10], lnm));
+  const double res = fma(de, kLogPoly[9], fma(de, kLogPoly[10], lnm));
+  return dsel(ok, res, __longlong_as_double(0x7ff8000000000000ll));
 }
 
 // Per-node record, all entries pre-scaled so that pair sums are exact means.
@@ -87,8 +89,8 @@ __device__ __forceinline__ void logmean_parts(double hx, double hy, double hlx, 
   const bool series = d2 < __dmul_rn(kLogMeanEps, s2);
   const double u = d2 * rcp_approx(s2);
   const double q = fma(u, fma(u, 1.0 / 7.0, 1.0 / 5.0), 1.0 / 3.0);
-  num = series ? s * s2 : d;
-  den = series ? fma(d2, q, s2) : __dsub_rn(hly, hlx);
+  num = dsel(series, s * s2, d);
+  den = dsel(series, fma(d2, q, s2), __dsub_rn(hly, hlx));
 }
 
 // Two-point flux between node records a and b for the (unnormalised)
