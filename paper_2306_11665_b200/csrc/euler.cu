@@ -67,7 +67,7 @@ struct EulerCartCfg {
   static constexpr int kThreads = 32 * (kLineWarps + kPrepWarps);
   static constexpr int kMinBlocks = (N == 4) ? SFB_MINBLOCKS_N4 : 1;
   static constexpr int kVals = kEPB * 5 * kNodes;  // doubles per block of states
-  static constexpr int kPlanes = 9;                // 8 record planes + pressure
+  static constexpr int kPlanes = 8;                // 7 record planes + pressure
   static constexpr int kRecVals = kPlanes * kEPB * kNodes;
   // smem (doubles): 2 input buffers + 2 record sets + 3 direction residuals + diag(D)
   static constexpr size_t kSmem = (size_t)(2 * kVals + 2 * kRecVals + 3 * kVals + 8) * sizeof(double);
@@ -131,8 +131,9 @@ __device__ __forceinline__ void chandrashekar_cart_k(const NodeRec* const (&A)[K
     f[k][1] = fma(f1, vb0[k], dsel(dir == 0, phat, 0.0));
     f[k][2] = fma(f1, vb1[k], dsel(dir == 1, phat, 0.0));
     f[k][3] = fma(f1, vb2[k], dsel(dir == 2, phat, 0.0));
-    const double vv = fma(vb2[k], vb2[k], fma(vb1[k], vb1[k], vb0[k] * vb0[k]));
-    const double g = fma(c_gamma, ibeta, vv - (A[k]->q + B[k]->q));
+    // |vbar|^2 - (|v_a|^2 + |v_b|^2)/4 = 2 (v_a/2).(v_b/2): no cancellation, no q plane
+    const double dot = fma(A[k]->hv2, B[k]->hv2, fma(A[k]->hv1, B[k]->hv1, A[k]->hv0 * B[k]->hv0));
+    const double g = fma(2.0, dot, c_gamma * ibeta);
     f[k][4] = fma(f1, g, phat * vn);
   }
 }
@@ -196,7 +197,7 @@ __device__ __forceinline__ void line_work(const double* __restrict__ rec, int el
     q.hb = p[4 * S];
     q.hlr = p[5 * S];
     q.hlb = p[6 * S];
-    q.q = p[7 * S];
+    q.q = 0.0;  // unused: the energy flux uses 2 (v_a/2).(v_b/2)
     return q;
   };
 #pragma unroll
@@ -331,7 +332,8 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
           const int qn = swz<N>(c0, c1, c2);
           const double* rc = rec + e * NN + qn;
           const double hr = rc[0], h0 = rc[S], h1 = rc[2 * S], h2 = rc[3 * S];
-          const double q = rc[7 * S], p = rc[8 * S];
+          const double p = rc[7 * S];
+          const double q = fma(h2, h2, fma(h1, h1, h0 * h0));  // |v|^2 / 4
           const double d0 = ddiag[c0], d1 = ddiag[c1], d2 = ddiag[c2];
           const double w = 2.0 * fma(d2, h2, fma(d1, h1, d0 * h0));  // sum_j d_j v_j
           const double rho = 2.0 * hr;
@@ -413,8 +415,7 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
         rec[4 * S + q] = 0.5 * beta;
         rec[5 * S + q] = 0.5 * log_pos(rho);
         rec[6 * S + q] = 0.5 * log_pos(beta);
-        rec[7 * S + q] = 0.25 * vv;
-        rec[8 * S + q] = p;
+        rec[7 * S + q] = p;
       }
       nbar_arrive(REC_FULL + s, kAll);
     }

@@ -67,7 +67,7 @@ struct NodeRec {
   double hb;       // beta / 2
   double hlr;      // ln(rho) / 2
   double hlb;      // ln(beta) / 2
-  double q;        // |v|^2 / 4
+  double q;        // |v|^2 / 4 (legacy; the flux uses 2 (v_a/2).(v_b/2))
 };
 
 // Numerator / denominator of the log mean of (x, y) = (2 hx, 2 hy):

@@ -118,8 +118,8 @@ __device__ __forceinline__ void chandrashekar_curv_k(const NodeRec (&A)[K],
     f[k][1] = fma(f1, vb0[k], phat * nx[k]);
     f[k][2] = fma(f1, vb1[k], phat * ny[k]);
     f[k][3] = fma(f1, vb2[k], phat * nz[k]);
-    const double vv = fma(vb2[k], vb2[k], fma(vb1[k], vb1[k], vb0[k] * vb0[k]));
-    const double g = fma(c_gamma, ibeta, vv - (A[k].q + B[k].q));
+    const double dot = fma(A[k].hv2, B[k].hv2, fma(A[k].hv1, B[k].hv1, A[k].hv0 * B[k].hv0));
+    const double g = fma(2.0, dot, c_gamma * ibeta);
     f[k][4] = fma(f1, g, phat * vn);
   }
 }
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads)
           q.hb = rec[4 * NN + k];
           q.hlr = rec[5 * NN + k];
           q.hlb = rec[6 * NN + k];
-          q.q = rec[7 * NN + k];
+          q.q = 0.0;
           return q;
         };
 #pragma unroll
