@@ -29,15 +29,16 @@
 //   pos(r0,r1,r2) = r2 N^2 + ((r0+r2) mod N) + N ((r1+r2) mod N)
 // which makes the stride-1, stride-N and stride-N^2 line accesses of all three
 // directions bank-conflict free for N = 4.
-#include "bulk.cuh"
-#include "common.cuh"
-#include "euler_flux.cuh"
+#include "euler_common.cuh"
 
 #ifndef SFB_PAIR_BATCH_N4
 #define SFB_PAIR_BATCH_N4 3
 #endif
 #ifndef SFB_MINBLOCKS_N4
 #define SFB_MINBLOCKS_N4 4
+#endif
+#ifndef SFB_SPLIT_N4
+#define SFB_SPLIT_N4 0
 #endif
 #ifndef SFB_RECS_IN_REGS
 #define SFB_RECS_IN_REGS 0
@@ -47,11 +48,6 @@
 #endif
 
 namespace sfb {
-
-template <int N>
-struct DMat {
-  double d[N * N];  // scale * D, row-major
-};
 
 template <int N>
 struct EulerCartCfg {
@@ -73,70 +69,6 @@ struct EulerCartCfg {
   static constexpr size_t kSmem = (size_t)(2 * kVals + 2 * kRecVals + 3 * kVals + 8) * sizeof(double);
   static constexpr bool kBulk = ((kVals * 8) % 16) == 0;
 };
-
-template <int N>
-__device__ __forceinline__ int swz(int r0, int r1, int r2) {
-  int a = r0 + r2;
-  a = a >= N ? a - N : a;
-  int b = r1 + r2;
-  b = b >= N ? b - N : b;
-  return r2 * N * N + a + N * b;
-}
-
-template <int N>
-__device__ __forceinline__ int swz_flat(int r) {
-  return swz<N>(r % N, (r / N) % N, r / (N * N));
-}
-
-// Cartesian Chandrashekar flux along direction dir (unit normal e_dir) for K
-// independent pairs at once.  Every statement is written across the K pairs so
-// the instruction stream carries K independent dependency chains: the FP64
-// pipe needs ~4 independent DFMAs in flight per warp to approach its peak
-// (DFMA latency ~9 cycles; tools/peaks/fp64_latency.cu), which warps alone
-// cannot supply.  The direction only selects operands (ALU selects).
-template <int K>
-__device__ __forceinline__ void chandrashekar_cart_k(const NodeRec* const (&A)[K],
-                                                     const NodeRec* const (&B)[K], int dir,
-                                                     double c_gamma, double (&f)[K][5]) {
-  double vb0[K], vb1[K], vb2[K], nr[K], dr[K], nb[K], db[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    vb0[k] = A[k]->hv0 + B[k]->hv0;
-    vb1[k] = A[k]->hv1 + B[k]->hv1;
-    vb2[k] = A[k]->hv2 + B[k]->hv2;
-  }
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    logmean_parts(A[k]->hr, B[k]->hr, A[k]->hlr, B[k]->hlr, nr[k], dr[k]);  // rho_ln
-    logmean_parts(A[k]->hb, B[k]->hb, A[k]->hlb, B[k]->hlb, nb[k], db[k]);  // beta_ln
-  }
-  double sr[K], sb[K], p1[K], rr[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    sr[k] = A[k]->hr + B[k]->hr;  // rhobar
-    sb[k] = A[k]->hb + B[k]->hb;  // betabar
-    p1[k] = dr[k] * nb[k];
-    rr[k] = rcp_refined(p1[k] * sb[k]);
-  }
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const double inv_sb = rr[k] * p1[k];
-    const double t = rr[k] * sb[k];
-    const double rho_ln = nr[k] * (t * nb[k]);
-    const double ibeta = db[k] * (t * dr[k]);
-    const double phat = 0.5 * sr[k] * inv_sb;
-    const double vn = dsel(dir == 0, vb0[k], dsel(dir == 1, vb1[k], vb2[k]));
-    const double f1 = rho_ln * vn;
-    f[k][0] = f1;
-    f[k][1] = fma(f1, vb0[k], dsel(dir == 0, phat, 0.0));
-    f[k][2] = fma(f1, vb1[k], dsel(dir == 1, phat, 0.0));
-    f[k][3] = fma(f1, vb2[k], dsel(dir == 2, phat, 0.0));
-    // |vbar|^2 - (|v_a|^2 + |v_b|^2)/4 = 2 (v_a/2).(v_b/2): no cancellation, no q plane
-    const double dot = fma(A[k]->hv2, B[k]->hv2, fma(A[k]->hv1, B[k]->hv1, A[k]->hv0 * B[k]->hv0));
-    const double g = fma(2.0, dot, c_gamma * ibeta);
-    f[k][4] = fma(f1, g, phat * vn);
-  }
-}
 
 // Pair order of one line: the circle-method round robin, so consecutive pairs
 // are disjoint (independent dependency chains and accumulators) - for N = 4:
@@ -168,6 +100,7 @@ constexpr int kPairBatch = (N == 4) ? SFB_PAIR_BATCH_N4 : 2;
 
 template <int N>
 struct LineOut {
+  int vplane[3];  // record-plane offsets of the rotated velocity components
   int pos[N];
   double acc[N][5];
 };
@@ -186,14 +119,16 @@ __device__ __forceinline__ void line_work(const double* __restrict__ rec, int el
     const int r2 = dir == 2 ? a : w;
     o.pos[a] = swz<N>(r0, r1, r2);
   }
+#pragma unroll
+  for (int m = 0; m < 3; ++m) o.vplane[m] = (1 + (dir + m) % 3) * S;
   const double* re = rec + el * NN;
   auto load = [&](int a) {
     NodeRec q;
     const double* p = re + o.pos[a];
     q.hr = p[0];
-    q.hv0 = p[S];
-    q.hv1 = p[2 * S];
-    q.hv2 = p[3 * S];
+    q.hv0 = p[o.vplane[0]];  // velocity rotated to (normal, t1, t2) of this direction
+    q.hv1 = p[o.vplane[1]];
+    q.hv2 = p[o.vplane[2]];
     q.hb = p[4 * S];
     q.hlr = p[5 * S];
     q.hlb = p[6 * S];
@@ -233,7 +168,7 @@ __device__ __forceinline__ void line_work(const double* __restrict__ rec, int el
 #endif
     }
     double f[K][5];
-    chandrashekar_cart_k<K>(A, B, dir, c_gamma, f);
+    chandrashekar_cart_k<K>(A, B, c_gamma, f);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       if (k0 + k >= P) break;
@@ -246,14 +181,6 @@ __device__ __forceinline__ void line_work(const double* __restrict__ rec, int el
       }
     }
   }
-}
-
-// named barriers (id 0 is __syncthreads)
-__device__ __forceinline__ void nbar_sync(int id, int count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-__device__ __forceinline__ void nbar_arrive(int id, int count) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
 // Warp-specialised persistent kernel.  Line warps (the FP64-heavy pair work
@@ -310,10 +237,17 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
       if (active) line_work<N>(rec, el, dir, L, Dm, c_gamma, o);
       if (active) {
         double* rs = resb + dir * kVals + el * 5 * NN;
+        // momentum components come back in the rotated frame: un-rotate by address
+        const int mp0 = (1 + dir % 3) * NN, mp1 = (1 + (dir + 1) % 3) * NN,
+                  mp2 = (1 + (dir + 2) % 3) * NN;
 #pragma unroll
-        for (int a = 0; a < N; ++a)
-#pragma unroll
-          for (int v = 0; v < 5; ++v) rs[o.pos[a] + v * NN] = o.acc[a][v];
+        for (int a = 0; a < N; ++a) {
+          rs[o.pos[a]] = o.acc[a][0];
+          rs[o.pos[a] + mp0] = o.acc[a][1];
+          rs[o.pos[a] + mp1] = o.acc[a][2];
+          rs[o.pos[a] + mp2] = o.acc[a][3];
+          rs[o.pos[a] + 4 * NN] = o.acc[a][4];
+        }
       }
       nbar_sync(LINE_ONLY, kLineT);  // all three direction residuals written
       // residual = diag + (R_0 + R_1) + R_2 per node; the diagonal term
@@ -450,12 +384,17 @@ static int launch_euler_cartesian(int64_t E, const double* Dh, double gamma, dou
   return check_launch("euler_volume_cartesian");
 }
 
+int launch_euler_cart4_split(int64_t E, const double* Dh, double gamma, double scale,
+                             const double* U, double* R, cudaStream_t s);
+
 int euler_cartesian_dispatch(int64_t E, int64_t n, const double* D_host, double gamma,
                              double scale, const double* U, double* R, cudaStream_t s) {
   switch (n) {
     case 2: return launch_euler_cartesian<2>(E, D_host, gamma, scale, U, R, s);
     case 3: return launch_euler_cartesian<3>(E, D_host, gamma, scale, U, R, s);
-    case 4: return launch_euler_cartesian<4>(E, D_host, gamma, scale, U, R, s);
+    case 4:
+      return SFB_SPLIT_N4 ? launch_euler_cart4_split(E, D_host, gamma, scale, U, R, s)
+                          : launch_euler_cartesian<4>(E, D_host, gamma, scale, U, R, s);
     case 5: return launch_euler_cartesian<5>(E, D_host, gamma, scale, U, R, s);
     case 6: return launch_euler_cartesian<6>(E, D_host, gamma, scale, U, R, s);
     case 7: return launch_euler_cartesian<7>(E, D_host, gamma, scale, U, R, s);

@@ -15,7 +15,7 @@
 // the current element is transformed, differenced and projected - all in
 // shared memory, so HBM sees exactly Uhat + Ja in and Rhat (+ 8 B) out.
 //   stage A  three sum-factorised passes of V (one per direction), thread per
-//            (variable, line), ping-ponging between the input slot and scratch;
+//            (variable, line), ping-ponging between the input slot and the residual buffer;
 //   stage B  thread per node: primitives, per-node logs, node record; the
 //            diagonal term sum_i D[r_i,r_i] F#(u_r,u_r; Ja^i(r)) into the
 //            residual (consistency: F#(u,u;n) = f(u).n);
@@ -27,6 +27,13 @@
 #include "bulk.cuh"
 #include "common.cuh"
 #include "euler_flux.cuh"
+
+#ifndef SFB_MODAL_MINBLOCKS_N6
+#define SFB_MODAL_MINBLOCKS_N6 2
+#endif
+#ifndef SFB_MODAL_BATCH_N6
+#define SFB_MODAL_BATCH_N6 3
+#endif
 
 namespace sfb {
 
@@ -48,10 +55,11 @@ struct ModalCfg {
   static constexpr int kU = 5 * kNodes;   // doubles of Uhat / u / r per element
   static constexpr int kJ = 9 * kNodes;   // doubles of Ja per element
   static constexpr int kSlot = kU + kJ;   // one input slot
-  static constexpr int kRec = 9 * kNodes; // node records: 8 planes + p
+  static constexpr int kRec = 8 * kNodes; // node records: 7 planes + p
   static constexpr int kRedPow2 = kThreads <= 128 ? 128 : (kThreads <= 256 ? 256 : 512);
   static constexpr size_t kSmem =
-      (size_t)(2 * kSlot + kU /*scratch*/ + kRec + kU /*residual*/ + kRedPow2) * sizeof(double);
+      (size_t)(2 * kSlot + kRec + kU /*residual*/ + kRedPow2) * sizeof(double);
+  static constexpr int kMinBlocks = (N == 6) ? SFB_MODAL_MINBLOCKS_N6 : 1;
 };
 
 // one sum-factorised pass along direction j: out[.., a_j, ..] = sum_c A[a_j][c] in[.., c, ..]
@@ -145,10 +153,10 @@ struct ModalPairs {
 };
 
 template <int N>
-constexpr int kModalBatch = (N >= 7) ? 1 : (N == 6 ? 3 : (N >= 4 ? 2 : 1));
+constexpr int kModalBatch = (N >= 7) ? 1 : (N == 6 ? SFB_MODAL_BATCH_N6 : (N >= 4 ? 2 : 1));
 
 template <int N>
-__global__ void __launch_bounds__(ModalCfg<N>::kThreads)
+__global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks)
     euler_modal_kernel(int64_t E, const ModalOps<N> ops, double gm1, double c_gamma,
                        double gam_ratio, const double* __restrict__ Uhat,
                        const double* __restrict__ Ja, double* __restrict__ Rhat,
@@ -157,10 +165,12 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads)
   constexpr int NN = Cfg::kNodes;
   constexpr int T = Cfg::kThreads;
   extern __shared__ __align__(16) double smem[];
+  // smem: 2 input slots [Uhat | Ja], node records, residual.  The slot's Uhat
+  // region doubles as the transform ping-pong buffer: V^3 runs slot -> res ->
+  // slot -> res (u ends in res), Pi^3 runs res -> slot -> res -> slot.
   double* slots = smem;                    // [2][Uhat | Ja]
-  double* scratch = smem + 2 * Cfg::kSlot; // [5][NN]
-  double* rec = scratch + Cfg::kU;         // [9][NN] node records (natural layout)
-  double* res = rec + Cfg::kRec;           // [5][NN] nodal residual r
+  double* rec = smem + 2 * Cfg::kSlot;     // [8][NN] node records (natural layout)
+  double* res = rec + Cfg::kRec;           // [5][NN] u, then the nodal residual r
   double* red = res + Cfg::kU;             // [T] reduction scratch
   __shared__ uint64_t full[2];
   __shared__ double sops[3 * N * N + N];
@@ -215,16 +225,16 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads)
     }
 
     // ---- stage A: u = V^3 Uhat ------------------------------------------------
-    kron_pass<N>(sV, 0, in, scratch, tid, T);
+    kron_pass<N>(sV, 0, in, res, tid, T);
     __syncthreads();
-    kron_pass<N>(sV, 1, scratch, in, tid, T);
+    kron_pass<N>(sV, 1, res, in, tid, T);
     __syncthreads();
-    kron_pass<N>(sV, 2, in, scratch, tid, T);  // u in scratch
+    kron_pass<N>(sV, 2, in, res, tid, T);  // u in res
     __syncthreads();
 
     // ---- stage B: node records + diagonal term ----------------------------------
     for (int r = tid; r < NN; r += T) {
-      const double* u = scratch + r;
+      const double* u = res + r;  // read this node's u, then overwrite it with its diagonal term
       const double rho = u[0], m0 = u[NN], m1 = u[2 * NN], m2 = u[3 * NN], et = u[4 * NN];
       const double irho = rcp_refined(rho);
       const double v0 = m0 * irho, v1 = m1 * irho, v2 = m2 * irho;
@@ -238,8 +248,7 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads)
       rec[4 * NN + r] = 0.5 * beta;
       rec[5 * NN + r] = 0.5 * log_pos(rho);
       rec[6 * NN + r] = 0.5 * log_pos(beta);
-      rec[7 * NN + r] = 0.25 * vv;
-      rec[8 * NN + r] = p;
+      rec[7 * NN + r] = p;
       // n_diag = sum_i D[r_i,r_i] Ja^i(r)
       const int c0 = r % N, c1 = (r / N) % N, c2 = r / (N * N);
       const double d0 = sDd[c0], d1 = sDd[c1], d2 = sDd[c2];
@@ -334,16 +343,16 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads)
     }
 
     // ---- stage D: Rhat = Pi^3 r, store, sum of squares -------------------------
-    kron_pass<N>(sP, 0, res, scratch, tid, T);
+    kron_pass<N>(sP, 0, res, in, tid, T);
     __syncthreads();
-    kron_pass<N>(sP, 1, scratch, res, tid, T);
+    kron_pass<N>(sP, 1, in, res, tid, T);
     __syncthreads();
-    kron_pass<N>(sP, 2, res, scratch, tid, T);  // Rhat in scratch
+    kron_pass<N>(sP, 2, res, in, tid, T);  // Rhat in the slot's Uhat region
     __syncthreads();
     double* Rg = Rhat + e * Cfg::kU;
     double ss = 0.0;
     for (int i = tid; i < Cfg::kU; i += T) {
-      const double x = scratch[i];
+      const double x = in[i];
       __stcs(Rg + i, x);
       ss = fma(x, x, ss);
     }
