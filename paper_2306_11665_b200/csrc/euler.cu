@@ -55,19 +55,20 @@ struct EulerCartCfg {
   static constexpr int kLines = N * N;
   // elements per block; line threads = 3 EPB N^2 (padded to warps), chosen so
   // the padding is small and the line warps are direction-uniform for N = 4
-  static constexpr int kEPB = (N == 2) ? 8 : (N == 3) ? 7 : (N == 7 || N == 8) ? 1 : 2;
+  // (EPB*5*N^3*8 bytes must be a multiple of 16 for the 1-D bulk copy)
+  static constexpr int kEPB = (N == 2) ? 8 : (N == 3) ? 8 : (N >= 7) ? 1 : 2;
   static constexpr int kLineThreads = 3 * kLines * kEPB;
   static constexpr int kLineWarps = (kLineThreads + 31) / 32;
   // prep warps balance node preprocessing + stores against the line work
   static constexpr int kPrepWarps = (N <= 3) ? 3 : (N == 4 ? SFB_PREP_WARPS_N4 : 1);
   static constexpr int kThreads = 32 * (kLineWarps + kPrepWarps);
-  static constexpr int kMinBlocks = (N == 4) ? SFB_MINBLOCKS_N4 : 1;
+  static constexpr int kMinBlocks = (N == 4) ? SFB_MINBLOCKS_N4 : ((N == 5 || N == 3 || N == 7) ? 2 : 1);
   static constexpr int kVals = kEPB * 5 * kNodes;  // doubles per block of states
   static constexpr int kPlanes = 8;                // 7 record planes + pressure
   static constexpr int kRecVals = kPlanes * kEPB * kNodes;
   // smem (doubles): 2 input buffers + 2 record sets + 3 direction residuals + diag(D)
-  static constexpr size_t kSmem = (size_t)(2 * kVals + 2 * kRecVals + 3 * kVals + 8) * sizeof(double);
-  static constexpr bool kBulk = ((kVals * 8) % 16) == 0;
+  static constexpr int kSlot = (kVals + 3) / 2 * 2;  // input slot: +1 double of alignment shift, kept even (16-B aligned slots)
+  static constexpr size_t kSmem = (size_t)(2 * kSlot + 2 * kRecVals + 3 * kVals + 8) * sizeof(double);
 };
 
 // Pair order of one line: the circle-method round robin, so consecutive pairs
@@ -96,7 +97,7 @@ struct PairOrder {
 
 // pairs evaluated side by side per line thread (ILP knob)
 template <int N>
-constexpr int kPairBatch = (N == 4) ? SFB_PAIR_BATCH_N4 : 2;
+constexpr int kPairBatch = (N == 4) ? SFB_PAIR_BATCH_N4 : ((N == 5 || N == 7) ? 1 : 2);
 
 template <int N>
 struct LineOut {
@@ -205,7 +206,8 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
   enum { REC_FULL = 1, REC_EMPTY = 3, LINE_ONLY = 5, PREP_ONLY = 6 };
   extern __shared__ __align__(16) double smem[];
   double* ibuf = smem;                      // [2][EPB][5][NN] bulk-copy target
-  double* recb = smem + 2 * kVals;          // [2][13][EPB*NN] swizzled records + diagonal
+  constexpr int kSlot = Cfg::kSlot;
+  double* recb = smem + 2 * kSlot;          // [2][8][EPB*NN] swizzled records + p
   double* resb = recb + 2 * Cfg::kRecVals;  // [3][EPB][5][NN] swizzled direction residuals
   double* ddiag = resb + 3 * kVals;         // [N] scale*D[i][i]
   __shared__ uint64_t full[2];
@@ -290,16 +292,26 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
   } else {
     // =========================== prep warps ==================================
     const int pt = tid - kLineT;
-    auto block_bytes = [&](int64_t blk) {
+    // A block's states start at double offset blk*EPB*5*NN, which is odd for
+    // odd 5*N^3*EPB: the bulk copy then starts one double early (16-byte
+    // alignment) and the block is read at `shift` = 1.  Only a final block whose
+    // aligned copy would run past the end of U falls back to plain loads.
+    const int64_t total_vals = E * 5 * NN;
+    auto block_shift = [&](int64_t blk) { return (int)((blk * EPB * 5 * NN) & 1); };
+    auto block_vals = [&](int64_t blk) {
       const int64_t e0 = blk * EPB;
       const int nel = (E - e0) < EPB ? (int)(E - e0) : EPB;
-      return (uint32_t)nel * 5 * NN * 8;
+      return nel * 5 * NN;
     };
-    auto bulk_ok = [&](int64_t blk) { return Cfg::kBulk && (block_bytes(blk) % 16) == 0; };
+    auto copy_doubles = [&](int64_t blk) { return (block_shift(blk) + block_vals(blk) + 1) & ~1; };
+    auto bulk_ok = [&](int64_t blk) {
+      return blk * EPB * 5 * NN - block_shift(blk) + copy_doubles(blk) <= total_vals;
+    };
     auto issue = [&](int64_t blk, int slot) {
-      const uint32_t bytes = block_bytes(blk);
+      const uint32_t bytes = (uint32_t)copy_doubles(blk) * 8;
       mbar_arrive_expect_tx(&full[slot], bytes);
-      bulk_g2s(ibuf + slot * kVals, U + blk * EPB * 5 * NN, bytes, &full[slot]);
+      bulk_g2s(ibuf + slot * kSlot, U + blk * EPB * 5 * NN - block_shift(blk), bytes,
+               &full[slot]);
     };
     int64_t blk = blockIdx.x;
     if (pt == 0 && niter > 0 && bulk_ok(blk)) issue(blk, 0);
@@ -309,7 +321,7 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
       const int s = it & 1;
       const int64_t e0 = blk * EPB;
       const int nel = (E - e0) < EPB ? (int)(E - e0) : EPB;
-      double* in = ibuf + slot * kVals;
+      double* in = ibuf + slot * kSlot;
       // all prep threads are done reading the other input slot (block it-1)
       nbar_sync(PREP_ONLY, kPrepT);
       const int64_t nxt = blk + gridDim.x;
@@ -320,7 +332,8 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
       if (bulk_ok(blk)) {
         mbar_wait_parity(&full[slot], (parity_bits >> slot) & 1u);
         parity_bits ^= 1u << slot;
-      } else {  // odd-sized tail: plain loads
+        in += block_shift(blk);
+      } else {  // final block that cannot be copied aligned: plain loads
         for (int i = pt; i < nel * 5 * NN; i += kPrepT) in[i] = __ldcs(U + e0 * 5 * NN + i);
         nbar_sync(PREP_ONLY, kPrepT);
       }

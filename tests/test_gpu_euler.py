@@ -146,3 +146,18 @@ def test_burgers_flop_count_and_batched():
     for e in range(9):
         ref = sf.volume_residual(sf.BurgersState(3, 3, u[e].cpu().numpy()))
         assert np.array_equal(out[e], ref)
+
+
+@pytest.mark.parametrize("n", [3, 5, 7])
+def test_many_blocks_per_cta_odd_sizes(n):
+    # odd 5 n^3: element blocks start at odd double offsets, so the bulk copy is
+    # shifted by one double; enough elements that every CTA loops over both
+    # input slots, and a ragged tail that takes the plain-load path
+    E = {3: 40001, 5: 12001, 7: 4001}[n]
+    U = eu.generate_states(E, n, seed=90 + n)
+    R = eu.volume_cartesian(U, n)
+    _, D, _, _ = eu.gll_operators(n)
+    idx = np.concatenate([np.arange(3), np.random.default_rng(n).choice(E, 40, replace=False),
+                          np.arange(E - 3, E)])
+    ref = eo.euler_volume_cartesian(U[idx].cpu().numpy(), D)
+    assert max_rel(R[idx].cpu().numpy(), ref) <= TOL
