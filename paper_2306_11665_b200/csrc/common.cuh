@@ -64,6 +64,25 @@ __device__ __forceinline__ double2 ld_stream_d2(const double* p) {
   return v;
 }
 
+// 256-bit loads (LDG.E.ENL2.256, sm_100): one request per 32 B row segment.
+struct d4 {
+  double x, y, z, w;
+};
+__device__ __forceinline__ d4 ld_stream_d4(const double* p) {
+  d4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ d4 ld_ro_d4(const double* p) {
+  d4 v;
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+      : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ void st_stream_d2(double* p, double2 v) {
   asm volatile("st.global.L1::no_allocate.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y)
                : "memory");

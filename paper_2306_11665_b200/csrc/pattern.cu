@@ -206,34 +206,54 @@ __global__ void row_sum_kernel(const double* __restrict__ p, int64_t rows, int64
 // element-independent basis factor (L1/L2 resident) with separately rounded
 // products, sums in numpy order, then accumulates over j sequentially.
 // --------------------------------------------------------------------------
-template <int N>
+template <int N, int D>
 __global__ void __launch_bounds__(256) hadamard_rowsum_fixed_kernel(
-    int64_t E, int64_t R, int d, const double* __restrict__ basis,
-    const double* __restrict__ F, double* __restrict__ out_dir, double* __restrict__ out_sum) {
+    int64_t E, int64_t R, const double* __restrict__ basis, const double* __restrict__ F,
+    double* __restrict__ out_dir, double* __restrict__ out_sum) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t total = E * R;
+  const int64_t total = E * R;
   for (; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t e = t / R;
-    int64_t row = t - e * R;
-    double acc = 0.0;
-    for (int j = 0; j < d; ++j) {
-      const double* f = F + ((e * d + j) * R + row) * N;
+    const int64_t e = t / R;
+    const int64_t row = t - e * R;
+    // issue every direction's loads before any arithmetic: D*N*8 bytes in
+    // flight per thread (memory-level parallelism for an HBM-bound stream)
+    double fv[D][N], bv[D][N];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const double* f = F + ((e * D + j) * R + row) * N;
       const double* b = basis + ((int64_t)j * R + row) * N;
-      double p[N];
-      if constexpr (N % 2 == 0) {
+      if constexpr (N % 4 == 0) {
+#pragma unroll
+        for (int l = 0; l < N; l += 4) {
+          const d4 v = ld_stream_d4(f + l);
+          const d4 w = ld_ro_d4(b + l);
+          fv[j][l] = v.x; fv[j][l + 1] = v.y; fv[j][l + 2] = v.z; fv[j][l + 3] = v.w;
+          bv[j][l] = w.x; bv[j][l + 1] = w.y; bv[j][l + 2] = w.z; bv[j][l + 3] = w.w;
+        }
+      } else if constexpr (N % 2 == 0) {
 #pragma unroll
         for (int l = 0; l < N; l += 2) {
-          double2 v = ld_stream_d2(f + l);
-          double2 w = __ldg(reinterpret_cast<const double2*>(b + l));
-          p[l] = __dmul_rn(w.x, v.x);
-          p[l + 1] = __dmul_rn(w.y, v.y);
+          const double2 v = ld_stream_d2(f + l);
+          const double2 w = __ldg(reinterpret_cast<const double2*>(b + l));
+          fv[j][l] = v.x; fv[j][l + 1] = v.y;
+          bv[j][l] = w.x; bv[j][l + 1] = w.y;
         }
       } else {
 #pragma unroll
-        for (int l = 0; l < N; ++l) p[l] = __dmul_rn(__ldg(b + l), __ldcs(f + l));
+        for (int l = 0; l < N; ++l) {
+          fv[j][l] = __ldcs(f + l);
+          bv[j][l] = __ldg(b + l);
+        }
       }
-      double s = numpy_sum_small([&p](int i) { return p[i]; }, N);
-      if (out_dir) out_dir[(e * d + j) * R + row] = s;
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double p[N];
+#pragma unroll
+      for (int l = 0; l < N; ++l) p[l] = __dmul_rn(bv[j][l], fv[j][l]);
+      const double s = numpy_sum_small([&p](int i) { return p[i]; }, N);
+      if (out_dir) out_dir[(e * D + j) * R + row] = s;
       acc = (j == 0) ? s : __dadd_rn(acc, s);
     }
     if (out_sum) out_sum[t] = acc;
@@ -394,20 +414,16 @@ extern "C" int sfb_hadamard_rowsum_batched(int64_t E, int64_t m, int64_t n, int6
   int threads = 256;
   int64_t blocks64 = (total + threads - 1) / threads;
   int blocks = (int)(blocks64 > (1 << 30) ? (1 << 30) : blocks64);
-  bool aligned = (((uintptr_t)F | (uintptr_t)basis) % 16) == 0;
-  switch (aligned ? n : 0) {
-    case 2:
-      hadamard_rowsum_fixed_kernel<2><<<blocks, threads, 0, s>>>(E, R, (int)d, basis, F, out_dir, out_sum);
-      break;
-    case 4:
-      hadamard_rowsum_fixed_kernel<4><<<blocks, threads, 0, s>>>(E, R, (int)d, basis, F, out_dir, out_sum);
-      break;
-    case 6:
-      hadamard_rowsum_fixed_kernel<6><<<blocks, threads, 0, s>>>(E, R, (int)d, basis, F, out_dir, out_sum);
-      break;
-    case 8:
-      hadamard_rowsum_fixed_kernel<8><<<blocks, threads, 0, s>>>(E, R, (int)d, basis, F, out_dir, out_sum);
-      break;
+  bool aligned = (((uintptr_t)F | (uintptr_t)basis) % 32) == 0;
+  const int key = aligned ? (int)(n * 10 + d) : 0;
+  switch (key) {
+    case 23: hadamard_rowsum_fixed_kernel<2, 3><<<blocks, threads, 0, s>>>(E, R, basis, F, out_dir, out_sum); break;
+    case 33: hadamard_rowsum_fixed_kernel<3, 3><<<blocks, threads, 0, s>>>(E, R, basis, F, out_dir, out_sum); break;
+    case 43: hadamard_rowsum_fixed_kernel<4, 3><<<blocks, threads, 0, s>>>(E, R, basis, F, out_dir, out_sum); break;
+    case 42: hadamard_rowsum_fixed_kernel<4, 2><<<blocks, threads, 0, s>>>(E, R, basis, F, out_dir, out_sum); break;
+    case 52: hadamard_rowsum_fixed_kernel<5, 2><<<blocks, threads, 0, s>>>(E, R, basis, F, out_dir, out_sum); break;
+    case 63: hadamard_rowsum_fixed_kernel<6, 3><<<blocks, threads, 0, s>>>(E, R, basis, F, out_dir, out_sum); break;
+    case 83: hadamard_rowsum_fixed_kernel<8, 3><<<blocks, threads, 0, s>>>(E, R, basis, F, out_dir, out_sum); break;
     default:
       hadamard_rowsum_generic_kernel<<<grid_for(total, threads), threads, 0, s>>>(
           E, R, n, (int)d, basis, F, out_dir, out_sum);
