@@ -32,16 +32,19 @@
 #include "euler_common.cuh"
 
 #ifndef SFB_PAIR_BATCH_N4
-#define SFB_PAIR_BATCH_N4 3
+#define SFB_PAIR_BATCH_N4 2
 #endif
 #ifndef SFB_MINBLOCKS_N4
 #define SFB_MINBLOCKS_N4 4
+#endif
+#ifndef SFB_REC_SETS_N4
+#define SFB_REC_SETS_N4 3
 #endif
 #ifndef SFB_SPLIT_N4
 #define SFB_SPLIT_N4 0
 #endif
 #ifndef SFB_RECS_IN_REGS
-#define SFB_RECS_IN_REGS 0
+#define SFB_RECS_IN_REGS 1
 #endif
 #ifndef SFB_PREP_WARPS_N4
 #define SFB_PREP_WARPS_N4 1
@@ -68,7 +71,8 @@ struct EulerCartCfg {
   static constexpr int kRecVals = kPlanes * kEPB * kNodes;
   // smem (doubles): 2 input buffers + 2 record sets + 3 direction residuals + diag(D)
   static constexpr int kSlot = (kVals + 3) / 2 * 2;  // input slot: +1 double of alignment shift, kept even (16-B aligned slots)
-  static constexpr size_t kSmem = (size_t)(2 * kSlot + 2 * kRecVals + 3 * kVals + 8) * sizeof(double);
+  static constexpr int kRecSets = (N == 4) ? SFB_REC_SETS_N4 : 2;  // record-set ring depth
+  static constexpr size_t kSmem = (size_t)(2 * kSlot + kRecSets * kRecVals + 3 * kVals + 8) * sizeof(double);
 };
 
 // Pair order of one line: the circle-method round robin, so consecutive pairs
@@ -195,6 +199,7 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
     euler_cartesian_kernel(int64_t E, const DMat<N> Dm, double gm1, double c_gamma,
                            double gam_ratio, const double* __restrict__ U,
                            double* __restrict__ R) {
+  const double c_beta = c_gamma;  // 1 / (2 (gamma - 1))
   using Cfg = EulerCartCfg<N>;
   constexpr int NN = Cfg::kNodes;
   constexpr int EPB = Cfg::kEPB;
@@ -203,12 +208,13 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
   constexpr int kLineT = 32 * Cfg::kLineWarps;
   constexpr int kPrepT = 32 * Cfg::kPrepWarps;
   constexpr int kAll = kLineT + kPrepT;
-  enum { REC_FULL = 1, REC_EMPTY = 3, LINE_ONLY = 5, PREP_ONLY = 6 };
+  constexpr int RS = Cfg::kRecSets;
+  enum { REC_FULL = 1, REC_EMPTY = 4, LINE_ONLY = 7, PREP_ONLY = 8 };
   extern __shared__ __align__(16) double smem[];
   double* ibuf = smem;                      // [2][EPB][5][NN] bulk-copy target
   constexpr int kSlot = Cfg::kSlot;
   double* recb = smem + 2 * kSlot;          // [2][8][EPB*NN] swizzled records + p
-  double* resb = recb + 2 * Cfg::kRecVals;  // [3][EPB][5][NN] swizzled direction residuals
+  double* resb = recb + RS * Cfg::kRecVals;  // [3][EPB][5][NN] swizzled direction residuals
   double* ddiag = resb + 3 * kVals;         // [N] scale*D[i][i]
   __shared__ uint64_t full[2];
 
@@ -232,7 +238,7 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
     const int L = rem - el * Cfg::kLines;
     const bool active = tid < Cfg::kLineThreads;
     for (int it = 0; it < niter; ++it) {
-      const int s = it & 1;
+      const int s = it % RS;
       const double* rec = recb + s * Cfg::kRecVals;
       nbar_sync(REC_FULL + s, kAll);
       LineOut<N> o;
@@ -318,7 +324,7 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
     uint32_t parity_bits = 0;  // bit k = phase of input slot k (no local-memory array)
     for (int it = 0; it < niter; ++it, blk += gridDim.x) {
       const int slot = it & 1;
-      const int s = it & 1;
+      const int s = it % RS;
       const int64_t e0 = blk * EPB;
       const int nel = (E - e0) < EPB ? (int)(E - e0) : EPB;
       double* in = ibuf + slot * kSlot;
@@ -337,7 +343,7 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
         for (int i = pt; i < nel * 5 * NN; i += kPrepT) in[i] = __ldcs(U + e0 * 5 * NN + i);
         nbar_sync(PREP_ONLY, kPrepT);
       }
-      if (it >= 2) nbar_sync(REC_EMPTY + s, kAll);  // record set s read for block it-2
+      if (it >= RS) nbar_sync(REC_EMPTY + s, kAll);  // record set s read for block it-RS
       double* rec = recb + s * Cfg::kRecVals;
       constexpr int kPer = (S + kPrepT - 1) / kPrepT;
 #pragma unroll
@@ -348,11 +354,15 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
         const int r = i - el * NN;
         const double* u = in + el * 5 * NN + r;
         const double rho = u[0], m0 = u[NN], m1 = u[2 * NN], m2 = u[3 * NN], et = u[4 * NN];
+        // two independent reciprocals (1/rho and 1/X, X = rho E - |m|^2/2 = rho p/(gamma-1))
+        // instead of the chain 1/rho -> p -> 1/p: shorter critical path per node
         const double irho = rcp_refined(rho);
+        const double mm = fma(m2, m2, fma(m1, m1, m0 * m0));
+        const double X = fma(rho, et, -0.5 * mm);
+        const double iX = rcp_refined(X);
         const double v0 = m0 * irho, v1 = m1 * irho, v2 = m2 * irho;
-        const double vv = fma(v2, v2, fma(v1, v1, v0 * v0));
-        const double p = gm1 * fma(-0.5 * rho, vv, et);
-        const double beta = 0.5 * rho * rcp_refined(p);
+        const double p = gm1 * X * irho;
+        const double beta = (rho * rho) * (c_beta * iX);  // rho / (2p) = rho^2 / (2 (gamma-1) X)
         const int c0 = r % N, c1 = (r / N) % N, c2 = r / (N * N);
         const int q = el * NN + swz<N>(c0, c1, c2);
         rec[q] = 0.5 * rho;
@@ -366,8 +376,8 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
       }
       nbar_arrive(REC_FULL + s, kAll);
     }
-    // match the REC_EMPTY arrivals of the last (up to) two blocks
-    for (int k = niter - 2 > 0 ? niter - 2 : 0; k < niter; ++k) nbar_sync(REC_EMPTY + (k & 1), kAll);
+    // match the REC_EMPTY arrivals of the last (up to) RS blocks
+    for (int k = niter - RS > 0 ? niter - RS : 0; k < niter; ++k) nbar_sync(REC_EMPTY + k % RS, kAll);
   }
 }
 

@@ -51,9 +51,16 @@ __device__ __forceinline__ double log_pos(double x) {
   double f = num * r;
   f = fma(r, fma(-f, den, num), f);
   const double f2 = f * f;
-  double p = kLogPoly[8];
-#pragma unroll
-  for (int k = 7; k >= 0; --k) p = fma(p, f2, kLogPoly[k]);
+  // Estrin evaluation of the degree-8 polynomial in f2 (depth 4 instead of 8)
+  const double f4 = f2 * f2;
+  const double f8 = f4 * f4;
+  const double q01 = fma(kLogPoly[1], f2, kLogPoly[0]);
+  const double q23 = fma(kLogPoly[3], f2, kLogPoly[2]);
+  const double q45 = fma(kLogPoly[5], f2, kLogPoly[4]);
+  const double q67 = fma(kLogPoly[7], f2, kLogPoly[6]);
+  const double q03 = fma(q23, f4, q01);
+  const double q47 = fma(q67, f4, q45);
+  const double p = fma(fma(kLogPoly[8], f8, q47), f8, q03);
   const double lnm = fma(f * f2, p, f + f);
   const double de = (double)e;
   const double res = fma(de, kLogPoly[9], fma(de, kLogPoly[10], lnm));
