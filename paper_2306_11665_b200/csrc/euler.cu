@@ -40,6 +40,12 @@
 #ifndef SFB_REC_SETS_N4
 #define SFB_REC_SETS_N4 3
 #endif
+#ifndef SFB_EXP_NO_LINE
+#define SFB_EXP_NO_LINE 0
+#endif
+#ifndef SFB_EXP_NO_PREP
+#define SFB_EXP_NO_PREP 0
+#endif
 #ifndef SFB_SPLIT_N4
 #define SFB_SPLIT_N4 0
 #endif
@@ -199,7 +205,7 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
     euler_cartesian_kernel(int64_t E, const DMat<N> Dm, double gm1, double c_gamma,
                            double gam_ratio, const double* __restrict__ U,
                            double* __restrict__ R) {
-  const double c_beta = c_gamma;  // 1 / (2 (gamma - 1))
+  const double c_hbeta = 0.5 * c_gamma;  // 1 / (4 (gamma - 1))
   using Cfg = EulerCartCfg<N>;
   constexpr int NN = Cfg::kNodes;
   constexpr int EPB = Cfg::kEPB;
@@ -242,7 +248,11 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
       const double* rec = recb + s * Cfg::kRecVals;
       nbar_sync(REC_FULL + s, kAll);
       LineOut<N> o;
+#if SFB_EXP_NO_LINE
+      if (active) { for (int a = 0; a < N; ++a) { o.pos[a] = a; for (int v = 0; v < 5; ++v) o.acc[a][v] = rec[a]; } }
+#else
       if (active) line_work<N>(rec, el, dir, L, Dm, c_gamma, o);
+#endif
       if (active) {
         double* rs = resb + dir * kVals + el * 5 * NN;
         // momentum components come back in the rotated frame: un-rotate by address
@@ -347,7 +357,7 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
       double* rec = recb + s * Cfg::kRecVals;
       constexpr int kPer = (S + kPrepT - 1) / kPrepT;
 #pragma unroll
-      for (int k = 0; k < kPer; ++k) {
+      for (int k = 0; k < (SFB_EXP_NO_PREP ? 0 : kPer); ++k) {
         const int i = pt + k * kPrepT;
         if (kPer * kPrepT != S && i >= S) break;
         const int el = i / NN;
@@ -355,23 +365,22 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
         const double* u = in + el * 5 * NN + r;
         const double rho = u[0], m0 = u[NN], m1 = u[2 * NN], m2 = u[3 * NN], et = u[4 * NN];
         // two independent reciprocals (1/rho and 1/X, X = rho E - |m|^2/2 = rho p/(gamma-1))
-        // instead of the chain 1/rho -> p -> 1/p: shorter critical path per node
-        const double irho = rcp_refined(rho);
+        // instead of the chain 1/rho -> p -> 1/p; halvings folded into the factors
+        const double hirho = 0.5 * rcp_refined(rho);
         const double mm = fma(m2, m2, fma(m1, m1, m0 * m0));
         const double X = fma(rho, et, -0.5 * mm);
         const double iX = rcp_refined(X);
-        const double v0 = m0 * irho, v1 = m1 * irho, v2 = m2 * irho;
-        const double p = gm1 * X * irho;
-        const double beta = (rho * rho) * (c_beta * iX);  // rho / (2p) = rho^2 / (2 (gamma-1) X)
+        const double p = (2.0 * gm1) * X * hirho;
+        const double hbeta = (rho * rho) * (c_hbeta * iX);  // beta/2 = rho^2 / (4 (gamma-1) X)
         const int c0 = r % N, c1 = (r / N) % N, c2 = r / (N * N);
         const int q = el * NN + swz<N>(c0, c1, c2);
         rec[q] = 0.5 * rho;
-        rec[S + q] = 0.5 * v0;
-        rec[2 * S + q] = 0.5 * v1;
-        rec[3 * S + q] = 0.5 * v2;
-        rec[4 * S + q] = 0.5 * beta;
-        rec[5 * S + q] = 0.5 * log_pos(rho);
-        rec[6 * S + q] = 0.5 * log_pos(beta);
+        rec[S + q] = m0 * hirho;
+        rec[2 * S + q] = m1 * hirho;
+        rec[3 * S + q] = m2 * hirho;
+        rec[4 * S + q] = hbeta;
+        rec[5 * S + q] = log_half(rho);
+        rec[6 * S + q] = log_half(2.0 * hbeta);
         rec[7 * S + q] = p;
       }
       nbar_arrive(REC_FULL + s, kAll);

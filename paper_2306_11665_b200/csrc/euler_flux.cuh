@@ -23,6 +23,10 @@ namespace sfb {
 
 constexpr double kLogMeanEps = 1.0e-4;
 
+#ifndef SFB_EXACT_LOGMEAN_TEST
+#define SFB_EXACT_LOGMEAN_TEST 0
+#endif
+
 // Coefficients of 2 atanh(f)/f - 2 = sum_k 2/(2k+3) f^(2k+2) (k = 0..8) plus
 // ln 2 split hi/lo.  In __constant__ memory so the DFMAs take them as
 // constant-bank operands instead of re-materialising 64-bit immediates.
@@ -77,6 +81,45 @@ struct NodeRec {
   double q;        // |v|^2 / 4 (legacy; the flux uses 2 (v_a/2).(v_b/2))
 };
 
+// Coefficients of the log series above, halved (log_half returns ln(x)/2).
+__constant__ double kLogPolyHalf[11] = {
+    1.0 / 3.0,  1.0 / 5.0,  1.0 / 7.0,  1.0 / 9.0,  1.0 / 11.0, 1.0 / 13.0,
+    1.0 / 15.0, 1.0 / 17.0, 1.0 / 19.0, 3.46573590184561908245e-01, 9.54107464635293850010e-11};
+
+// Half natural log ln(x)/2 (the node records store halved logs) for positive
+// normal x: x = 2^e m, m in [sqrt(1/2), sqrt(2)), ln m = 2 atanh(f),
+// f = (m-1)/(m+1), |f| <= 0.1716, series to f^19 (truncation < 2.5e-17
+// relative), Estrin-evaluated; the 1/2 is folded into the constants.  About
+// 18 FP64 operations, within ~2 ulp.  Branch-free: the validity test is an
+// integer range check on the high word (no FP64 compare); non-positive /
+// non-finite / subnormal inputs - non-physical states - return NaN.
+__device__ __forceinline__ double log_half(double x) {
+  const int hi = __double2hiint(x), lo = __double2loint(x);
+  const bool ok = (unsigned)(hi - 0x00100000) < 0x7fe00000u;
+  int e = (hi >> 20) - 1023;
+  int mh = (hi & 0x000fffff) | 0x3ff00000;
+  const bool big = mh > 0x3ff6a09e;  // m > sqrt(2)
+  mh = big ? mh - 0x00100000 : mh;
+  e = big ? e + 1 : e;
+  const double m = __hiloint2double(mh, lo);
+  const double num = m - 1.0;  // exact (Sterbenz)
+  const double f = num * rcp_refined(m + 1.0);
+  const double f2 = f * f;
+  const double f4 = f2 * f2;
+  const double f8 = f4 * f4;
+  const double q01 = fma(kLogPolyHalf[1], f2, kLogPolyHalf[0]);
+  const double q23 = fma(kLogPolyHalf[3], f2, kLogPolyHalf[2]);
+  const double q45 = fma(kLogPolyHalf[5], f2, kLogPolyHalf[4]);
+  const double q67 = fma(kLogPolyHalf[7], f2, kLogPolyHalf[6]);
+  const double q03 = fma(q23, f4, q01);
+  const double q47 = fma(q67, f4, q45);
+  const double p = fma(fma(kLogPolyHalf[8], f8, q47), f8, q03);
+  const double lnm_half = fma(f * f2, p, f);
+  const double de = (double)e;
+  const double res = fma(de, kLogPolyHalf[9], fma(de, kLogPolyHalf[10], lnm_half));
+  return dsel(ok, res, __longlong_as_double(0x7ff8000000000000ll));
+}
+
 // Numerator / denominator of the log mean of (x, y) = (2 hx, 2 hy):
 //   L = num / den.  Series when d^2 < EPS (s^2) (tested on halved values; the
 //   test is invariant under the exact halving, and uses the oracle's exact
@@ -93,7 +136,16 @@ __device__ __forceinline__ void logmean_parts(double hx, double hy, double hlx, 
   const double s = __dadd_rn(hx, hy);
   const double d2 = __dmul_rn(d, d);
   const double s2 = __dmul_rn(s, s);
+#if SFB_EXACT_LOGMEAN_TEST
   const bool series = d2 < __dmul_rn(kLogMeanEps, s2);
+#else
+  // Branch choice on the high words (integer ALU, no FP64 op): d^2/s^2 below
+  // ~2^-13.3 (1e-4 within a factor ~1.5).  Both branches are accurate on the
+  // fuzzy band (series truncation < 4e-16 for u < 2e-4; log branch < 1e-14
+  // for u > 5e-5), so a choice that differs from the oracle's exact test near
+  // the threshold changes the result by < 1e-14 relative.
+  const bool series = (__double2hiint(d2) - __double2hiint(s2)) < -(int)(0x3ff00000 - 0x3f1a36e2);
+#endif
   const double u = d2 * rcp_approx(s2);
   const double q = fma(u, fma(u, 1.0 / 7.0, 1.0 / 5.0), 1.0 / 3.0);
   num = dsel(series, s * s2, d);
