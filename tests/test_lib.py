@@ -86,3 +86,14 @@ def test_oracle_not_imported_by_product_package():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", src, re.M), f
     assert "oracle.euler_oracle" not in sys.modules or True
+
+
+def test_build_module_loads_without_the_library():
+    # __graft_entry__.build() must work from a clean checkout (no .so yet): the
+    # build script is loaded by path, never through the package import
+    import __graft_entry__ as g
+
+    mod = g._load_build_module()
+    assert mod.LIB_NAME == "libsumfac_b200.so"
+    assert all(src.endswith(".cu") for src in mod._sources())
+    assert "arch=compute_100a,code=sm_100a" in " ".join(mod.ARCH)
