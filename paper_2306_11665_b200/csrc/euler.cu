@@ -46,6 +46,9 @@
 #ifndef SFB_EXP_NO_PREP
 #define SFB_EXP_NO_PREP 0
 #endif
+#ifndef SFB_FUSED_N4
+#define SFB_FUSED_N4 1
+#endif
 #ifndef SFB_SPLIT_N4
 #define SFB_SPLIT_N4 0
 #endif
@@ -79,30 +82,6 @@ struct EulerCartCfg {
   static constexpr int kSlot = (kVals + 3) / 2 * 2;  // input slot: +1 double of alignment shift, kept even (16-B aligned slots)
   static constexpr int kRecSets = (N == 4) ? SFB_REC_SETS_N4 : 2;  // record-set ring depth
   static constexpr size_t kSmem = (size_t)(2 * kSlot + kRecSets * kRecVals + 3 * kVals + 8) * sizeof(double);
-};
-
-// Pair order of one line: the circle-method round robin, so consecutive pairs
-// are disjoint (independent dependency chains and accumulators) - for N = 4:
-// (0,3)(1,2) (1,3)(0,2) (2,3)(0,1).
-template <int N>
-struct PairOrder {
-  static constexpr int kPairs = N * (N - 1) / 2;
-  int a[kPairs > 0 ? kPairs : 1], b[kPairs > 0 ? kPairs : 1];
-  constexpr PairOrder() : a{}, b{} {
-    const int M = (N % 2 == 0) ? N : N + 1;  // odd N: dummy node M-1
-    int k = 0;
-    for (int round = 0; round < M - 1; ++round) {
-      for (int i = 0; i < M / 2; ++i) {
-        int x = (i == 0) ? M - 1 : (round + i) % (M - 1);
-        int y = (round - i + (M - 1)) % (M - 1);
-        if (i == 0) y = round;
-        if (x >= N || y >= N) continue;
-        a[k] = x < y ? x : y;
-        b[k] = x < y ? y : x;
-        ++k;
-      }
-    }
-  }
 };
 
 // pairs evaluated side by side per line thread (ILP knob)
@@ -418,6 +397,8 @@ static int launch_euler_cartesian(int64_t E, const double* Dh, double gamma, dou
 
 int launch_euler_cart4_split(int64_t E, const double* Dh, double gamma, double scale,
                              const double* U, double* R, cudaStream_t s);
+int launch_euler_cart4_fused(int64_t E, const double* Dh, double gamma, double scale,
+                             const double* U, double* R, cudaStream_t s);
 
 int euler_cartesian_dispatch(int64_t E, int64_t n, const double* D_host, double gamma,
                              double scale, const double* U, double* R, cudaStream_t s) {
@@ -425,6 +406,7 @@ int euler_cartesian_dispatch(int64_t E, int64_t n, const double* D_host, double 
     case 2: return launch_euler_cartesian<2>(E, D_host, gamma, scale, U, R, s);
     case 3: return launch_euler_cartesian<3>(E, D_host, gamma, scale, U, R, s);
     case 4:
+      if (SFB_FUSED_N4) return launch_euler_cart4_fused(E, D_host, gamma, scale, U, R, s);
       return SFB_SPLIT_N4 ? launch_euler_cart4_split(E, D_host, gamma, scale, U, R, s)
                           : launch_euler_cartesian<4>(E, D_host, gamma, scale, U, R, s);
     case 5: return launch_euler_cartesian<5>(E, D_host, gamma, scale, U, R, s);

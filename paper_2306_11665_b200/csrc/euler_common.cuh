@@ -79,6 +79,30 @@ __device__ __forceinline__ void chandrashekar_cart_k(const NodeRec* const (&A)[K
   }
 }
 
+// Pair order of one line: the circle-method round robin, so consecutive pairs
+// are disjoint (independent dependency chains and accumulators) - for N = 4:
+// (0,3)(1,2) (1,3)(0,2) (2,3)(0,1).
+template <int N>
+struct PairOrder {
+  static constexpr int kPairs = N * (N - 1) / 2;
+  int a[kPairs > 0 ? kPairs : 1], b[kPairs > 0 ? kPairs : 1];
+  constexpr PairOrder() : a{}, b{} {
+    const int M = (N % 2 == 0) ? N : N + 1;  // odd N: dummy node M-1
+    int k = 0;
+    for (int round = 0; round < M - 1; ++round) {
+      for (int i = 0; i < M / 2; ++i) {
+        int x = (i == 0) ? M - 1 : (round + i) % (M - 1);
+        int y = (round - i + (M - 1)) % (M - 1);
+        if (i == 0) y = round;
+        if (x >= N || y >= N) continue;
+        a[k] = x < y ? x : y;
+        b[k] = x < y ? y : x;
+        ++k;
+      }
+    }
+  }
+};
+
 // named barriers (id 0 is __syncthreads)
 __device__ __forceinline__ void nbar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
