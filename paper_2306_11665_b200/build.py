@@ -68,14 +68,16 @@ def _compile(src, verbose):
     return obj
 
 
-def build_variant(out_path, defines):
+def build_variant(out_path, defines, extra_flags=()):
     """Build an experimental variant (extra -D flags) into out_path (tools/ sweeps)."""
-    bdir = os.path.join(ROOT, "build", "variant_" + "_".join(d.replace("=", "") for d in defines))
+    tag = "_".join(d.replace("=", "") for d in defines) + "_".join(
+        f.replace("-", "").replace("=", "") for f in extra_flags)
+    bdir = os.path.join(ROOT, "build", "variant_" + tag)
     os.makedirs(bdir, exist_ok=True)
     objs = []
     for src in _sources():
         obj = os.path.join(bdir, os.path.basename(src)[:-3] + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, *("-D" + d for d in defines), "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *extra_flags, *("-D" + d for d in defines), "-c", src, "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")
