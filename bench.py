@@ -308,6 +308,10 @@ def run_ours(args):
             line["e2e"] = measure_e2e(args, U)
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = measure_cpu_baseline(args, U)
+        if world == 1 and not args.no_extras:
+            del U, R
+            torch.cuda.empty_cache()
+            line["other_configs"] = measure_other_configs(args, dev, stream, sampler, dist)
     sampler.stop()
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -466,6 +470,38 @@ def run_modal(args, world, rank, dev, stream, sampler, dist):
     return line
 
 
+def measure_other_configs(args, dev, stream, sampler, dist):
+    """Configs 2, 4, 5 in the same run (N=1), summarised; full lines via --config."""
+    import copy
+
+    import torch
+
+    out = {}
+    for cfg in (2, 4, 5):
+        a = copy.copy(args)
+        a.config = cfg
+        a.steps = 10 if cfg != 5 else 5
+        a.warmup = 3
+        a.n = 6 if cfg == 5 else 4
+        a.elements = 2**21 if cfg == 5 else 262144
+        a.traffic = None
+        fn = {2: run_hadamard, 4: run_sweep, 5: run_modal}[cfg]
+        ln = fn(a, 1, 0, dev, stream, sampler, dist)
+        summary = {"workload": ln["config"]["workload"], "metric": ln["metric"],
+                   "value": ln["value"], "unit": ln["unit"], "ms_per_step": ln["ms_per_step"],
+                   "roofline": {k: ln["roofline"][k] for k in ("bound", "achieved", "peak", "unit",
+                                                              "frac")}}
+        if cfg == 4:
+            summary["sweep"] = [{k: p[k] for k in ("n", "elements", "ms_per_step", "ns_per_dof",
+                                                   "hbm_frac", "fp64_frac")} for p in ln["sweep"]]
+            summary["slope_time_per_dof_vs_n"] = ln["slope_time_per_dof_vs_n"]
+        if cfg == 5:
+            summary["residual_norm"] = ln["residual_norm"]
+        out[f"config{cfg}"] = summary
+        torch.cuda.empty_cache()
+    return out
+
+
 def measure_e2e(args, U_dev):
     """Through the C-ABI host-buffer entry: pinned host U in, pinned host R out."""
     import torch
@@ -530,6 +566,8 @@ def main(argv=None):
     ap.add_argument("--elements", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the configs 2/4/5 summaries appended to the default line")
     ap.add_argument("--cpu-sample", type=int, default=262144)
     ap.add_argument("--cpu-seconds", type=float, default=3.0)
     ap.add_argument("--traffic", type=float, default=None,
