@@ -46,6 +46,9 @@
 #ifndef SFB_EXP_NO_PREP
 #define SFB_EXP_NO_PREP 0
 #endif
+#ifndef SFB_WARP_N4
+#define SFB_WARP_N4 1  // warp-autonomous kernel (euler_warp.cu)
+#endif
 #ifndef SFB_FUSED_N4
 #define SFB_FUSED_N4 1
 #endif
@@ -400,12 +403,16 @@ int launch_euler_cart4_split(int64_t E, const double* Dh, double gamma, double s
 int launch_euler_cart4_fused(int64_t E, const double* Dh, double gamma, double scale,
                              const double* U, double* R, cudaStream_t s);
 
+int launch_euler_cart4_warp(int64_t E, const double* Dh, double gamma, double scale,
+                            const double* U, double* R, cudaStream_t s);
+
 int euler_cartesian_dispatch(int64_t E, int64_t n, const double* D_host, double gamma,
                              double scale, const double* U, double* R, cudaStream_t s) {
   switch (n) {
     case 2: return launch_euler_cartesian<2>(E, D_host, gamma, scale, U, R, s);
     case 3: return launch_euler_cartesian<3>(E, D_host, gamma, scale, U, R, s);
     case 4:
+      if (SFB_WARP_N4) return launch_euler_cart4_warp(E, D_host, gamma, scale, U, R, s);
       if (SFB_FUSED_N4) return launch_euler_cart4_fused(E, D_host, gamma, scale, U, R, s);
       return SFB_SPLIT_N4 ? launch_euler_cart4_split(E, D_host, gamma, scale, U, R, s)
                           : launch_euler_cartesian<4>(E, D_host, gamma, scale, U, R, s);

@@ -152,6 +152,75 @@ __device__ __forceinline__ void logmean_parts(double hx, double hy, double hlx, 
   den = dsel(series, fma(d2, q, s2), __dsub_rn(hly, hlx));
 }
 
+// Leaner log mean for the n = 4 warp kernel (FP64 is its bottleneck): the
+// series branch is taken for u = d^2/s^2 below ~1e-5 (instead of 1e-4), where
+// den = s^2 + d^2 (1/3 + u/5) is exact to the u^3/7 < 1e-15 truncation: one
+// DFMA fewer than the three-term series.  On the log branch the per-node log
+// difference loses at most ~|ln x| 1e-16 / (2|d/s|), |d/s| >= 3e-3 ->
+// < 4e-14 relative between 1e-5 and the oracle's 1e-4 threshold
+// (tests/test_gpu_euler.py::test_log_mean_branch_band_matches_oracle).
+// Measured alternatives that were slower: forming u/5 in FP32 (from the high
+// words, or with cvt) - the FP64 saved does not pay for the extra ALU work.
+__device__ __forceinline__ void logmean_parts_v2(double hx, double hy, double hlx, double hly,
+                                                 double& num, double& den) {
+  const double d = __dsub_rn(hy, hx);
+  const double s = __dadd_rn(hx, hy);
+  const double d2 = __dmul_rn(d, d);
+  const double s2 = __dmul_rn(s, s);
+  // u < ~1e-5 on the high words (hi(1e-5) = 0x3ee4f8b5), integer ALU only
+  const bool series = (__double2hiint(d2) - __double2hiint(s2)) < -(int)(0x3ff00000 - 0x3ee4f8b5);
+  const double q = fma(d2 * rcp_approx(s2), 0.2, 1.0 / 3.0);
+  num = dsel(series, s * s2, d);
+  den = dsel(series, fma(d2, q, s2), __dsub_rn(hly, hlx));
+}
+
+// Cartesian flux for K pairs on records whose beta entries are pre-scaled by
+// 1/c_gamma = 2 (gamma - 1) (hb = (gamma - 1) beta, hlb = ln(hb)/2): the log
+// mean then returns beta_ln / c_gamma, so its reciprocal is already
+// c_gamma / beta_ln, and betabar carries the same factor, absorbed into the
+// p_hat constant (gm1 = gamma - 1): p_hat = rhobar / (2 betabar) = gm1 rhobar / sb.
+template <int K>
+__device__ __forceinline__ void chandrashekar_cart_v2(const NodeRec* const (&A)[K],
+                                                      const NodeRec* const (&B)[K], double gm1,
+                                                      double (&f)[K][5]) {
+  double vb0[K], vb1[K], vb2[K], nr[K], dr[K], nb[K], db[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    vb0[k] = A[k]->hv0 + B[k]->hv0;
+    vb1[k] = A[k]->hv1 + B[k]->hv1;
+    vb2[k] = A[k]->hv2 + B[k]->hv2;
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    logmean_parts_v2(A[k]->hr, B[k]->hr, A[k]->hlr, B[k]->hlr, nr[k], dr[k]);  // rho_ln
+    logmean_parts_v2(A[k]->hb, B[k]->hb, A[k]->hlb, B[k]->hlb, nb[k], db[k]);  // beta_ln/c
+  }
+  double sr[K], sb[K], p1[K], rr[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    sr[k] = __dadd_rn(A[k]->hr, B[k]->hr);  // rhobar (CSE with the log mean's s)
+    sb[k] = __dadd_rn(A[k]->hb, B[k]->hb);  // betabar / c_gamma
+    p1[k] = dr[k] * nb[k];
+    rr[k] = rcp_refined(p1[k] * sb[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const double inv_sb = rr[k] * p1[k];
+    const double t = rr[k] * sb[k];
+    const double rho_ln = nr[k] * (t * nb[k]);
+    const double cibeta = db[k] * (t * dr[k]);  // c_gamma / beta_ln
+    const double phat = (gm1 * sr[k]) * inv_sb;
+    const double vn = vb0[k];
+    const double f1 = rho_ln * vn;
+    f[k][0] = f1;
+    f[k][1] = fma(f1, vb0[k], phat);
+    f[k][2] = f1 * vb1[k];
+    f[k][3] = f1 * vb2[k];
+    const double dot = fma(A[k]->hv2, B[k]->hv2, fma(A[k]->hv1, B[k]->hv1, A[k]->hv0 * B[k]->hv0));
+    f[k][4] = fma(f1, fma(2.0, dot, cibeta), phat * vn);
+  }
+}
+
 // Two-point flux between node records a and b for the (unnormalised)
 // direction vector (n0, n1, n2).  Output f[5].
 __device__ __forceinline__ void chandrashekar(const NodeRec& a, const NodeRec& b, double n0,

@@ -161,3 +161,21 @@ def test_many_blocks_per_cta_odd_sizes(n):
                           np.arange(E - 3, E)])
     ref = eo.euler_volume_cartesian(U[idx].cpu().numpy(), D)
     assert max_rel(R[idx].cpu().numpy(), ref) <= TOL
+
+
+def test_log_mean_branch_band_matches_oracle():
+    # element-wise perturbations of a constant state with amplitudes 1e-1..1e-7:
+    # neighbour ratios sweep u = (d/s)^2 through both log-mean branches and
+    # the band between the kernel's and the oracle's thresholds (1e-5 / 1e-4)
+    n, E = 4, 512
+    U = eu.generate_states(E, n, seed=21)
+    base = U[:, :, :1].clone()
+    amp = torch.logspace(-1, -7, E, dtype=torch.float64, device="cuda")[:, None, None]
+    U = base + amp * (U - base)
+    R = eu.volume_cartesian(U, n).cpu().numpy()
+    _, D, _, _ = eu.gll_operators(n)
+    ref = c_oracle.euler_volume_cartesian(U.cpu().numpy(), D, threads=8)
+    assert max_rel(R, ref) <= TOL
+    # per element against the flux scale (the residual itself shrinks with amp)
+    scale = np.abs(U.cpu().numpy()).max(axis=(1, 2)) ** 2
+    assert (np.abs(R - ref).max(axis=(1, 2)) <= 1e-13 * scale).all()
