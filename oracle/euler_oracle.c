@@ -24,12 +24,20 @@
 #include <stdlib.h>
 #include <string.h>
 
-#define LOGMEAN_EPS 1.0e-4
+/* series iff hi(d^2) - hi(s^2) < -(hi(1.0) - hi(1e-5)): the integer test on
+   the IEEE high words shared with euler_oracle.py and csrc/euler_flux.cuh */
+#define LOGMEAN_HI_GAP (0x3ff00000 - 0x3ee4f8b5)
+
+static int32_t hiword(double x) {
+  uint64_t b;
+  memcpy(&b, &x, 8);
+  return (int32_t)(b >> 32);
+}
 
 static double logmean(double x, double y, double lx, double ly) {
   double d = y - x;
   double s = x + y;
-  if (d * d < LOGMEAN_EPS * (s * s)) {
+  if (hiword(d * d) - hiword(s * s) < -LOGMEAN_HI_GAP) {
     double u = (d * d) / (s * s);
     return s / (2.0 + u * (2.0 / 3.0 + u * (2.0 / 5.0 + u * (2.0 / 7.0))));
   }

@@ -8,24 +8,22 @@
 //   F1 = rho_ln vbar.n ;  F_{1+m} = F1 vbar_m + p_hat n_m
 //   F5 = F1 (1/(2(gamma-1) beta_ln) - (|v_a|^2 + |v_b|^2)/4) + sum_m vbar_m F_{1+m}
 // with L the logarithmic mean:
-//   d = y - x, s = x + y;  if d*d < EPS*(s*s):  L = s / (2 + u(2/3 + u(2/5 + u 2/7))), u = d^2/s^2
-//                          else:              L = d / (ln y - ln x)
-// The branch test is evaluated with the same IEEE operations (no FMA) as the
-// oracle, so both always take the same branch.  The kernel works on the halved
-// quantities x/2 (exact scaling), uses per-node logarithms and folds the three
-// per-pair reciprocals (1/L_rho, L_beta, 1/(2 betabar)) into one refined
-// reciprocal; these change rounding only (few ulps), never the branch.
+//   d = y - x, s = x + y, u = d^2/s^2;
+//   if hi(d^2) - hi(s^2) < -(hi(1) - hi(1e-5)):  L = s / (2 + u(2/3 + ...))
+//   else:                                        L = d / (ln y - ln x)
+// The branch test is the same integer comparison of IEEE high words as the
+// oracle's (oracle/euler_oracle.py:series_branch), so both take the same
+// branch.  The kernels work on rescaled quantities (x/2, or (gamma-1) beta),
+// use per-node logarithms and fold the three per-pair reciprocals
+// (1/L_rho, L_beta, 1/(2 betabar)) into one refined reciprocal; these change
+// rounding only (few ulps).
 #pragma once
 
 #include "common.cuh"
+#include "log_table.cuh"
 
 namespace sfb {
 
-constexpr double kLogMeanEps = 1.0e-4;
-
-#ifndef SFB_EXACT_LOGMEAN_TEST
-#define SFB_EXACT_LOGMEAN_TEST 0
-#endif
 
 // Coefficients of 2 atanh(f)/f - 2 = sum_k 2/(2k+3) f^(2k+2) (k = 0..8) plus
 // ln 2 split hi/lo.  In __constant__ memory so the DFMAs take them as
@@ -120,54 +118,60 @@ __device__ __forceinline__ double log_half(double x) {
   return dsel(ok, res, __longlong_as_double(0x7ff8000000000000ll));
 }
 
-// Numerator / denominator of the log mean of (x, y) = (2 hx, 2 hy):
-//   L = num / den.  Series when d^2 < EPS (s^2) (tested on halved values; the
-//   test is invariant under the exact halving, and uses the oracle's exact
-//   IEEE operations so both take the same branch).
-//   log branch:     num = d,        den = (ln y - ln x)/2       (per-node logs)
-//   series branch:  num = s s^2,    den = s^2 + d^2 Q(u),  Q = 1/3 + u/5 + u^2/7
-// i.e. s / (1 + u Q(u)) scaled by s^2 so that u = d^2/s^2 is only needed
-// inside Q, where a raw MUFU reciprocal (rel. err ~2^-22) costs < 1e-15
-// relative (u < 1e-4).  The final division happens in the caller's combined
-// reciprocal.
+// Table-driven ln(x)/2 for the n = 4 warp kernel's node records (~12 FP64
+// operations instead of log_half's ~22 and no reciprocal): after the same
+// reduction x = 2^e m, m in [sqrt(1/2), sqrt(2)), the top mantissa bits pick
+// c ~ 1/m from a 129-entry table (tools/gen_log_table.py; c = 1 next to
+// m = 1), r = m c - 1 is formed by one FMA (|r| <= 2^-7), and
+// ln(x)/2 = e ln2/2 + (-ln c)/2 + log1p(r)/2 with the series to r^8
+// (truncation < 1e-20).  Absolute error ~1e-17 (the log mean only uses
+// differences of these).  Non-positive / non-finite / subnormal -> NaN.
+static __device__ __align__(16) const double kLogTab[2 * SFB_LOG_TABLE_N] = {SFB_LOG_TABLE_VALUES};
+__device__ __forceinline__ double log_half_tab(double x) {
+  const int hi = __double2hiint(x), lo = __double2loint(x);
+  const bool ok = (unsigned)(hi - 0x00100000) < 0x7fe00000u;
+  int e = (hi >> 20) - 1023;
+  int mh = (hi & 0x000fffff) | 0x3ff00000;
+  const bool big = mh > 0x3ff6a09e;  // m > sqrt(2)
+  mh = big ? mh - 0x00100000 : mh;
+  e = big ? e + 1 : e;
+  int idx = (mh - SFB_LOG_TABLE_BASE) >> 13;
+  idx = min(max(idx, 0), SFB_LOG_TABLE_N - 1);
+  const double2 t = __ldg(reinterpret_cast<const double2*>(kLogTab) + idx);
+  const double rh = fma(__hiloint2double(mh, lo), 0.5 * t.x, -0.5);  // r/2, one rounding
+  const double r2 = rh * rh;
+  // log1p(2 rh)/2 = rh - rh^2 + 4/3 rh^3 - 2 rh^4 + 16/5 rh^5 - 16/3 rh^6 + 64/7 rh^7 - 16 rh^8
+  double p = fma(rh, -16.0, 64.0 / 7.0);
+  p = fma(rh, p, -16.0 / 3.0);
+  p = fma(rh, p, 16.0 / 5.0);
+  p = fma(rh, p, -2.0);
+  p = fma(rh, p, 4.0 / 3.0);
+  p = fma(rh, p, -1.0);
+  const double l1p = fma(r2, p, rh);
+  const double de = (double)e;
+  const double res = fma(de, kLogPolyHalf[9], fma(de, kLogPolyHalf[10], l1p + t.y));
+  return dsel(ok, res, __longlong_as_double(0x7ff8000000000000ll));
+}
+
+// Numerator / denominator of the log mean of (x, y) = (2 hx, 2 hy) (or any
+// exact rescaling): L = num / den.
+//   series branch:  num = s s^2,  den = s^2 + d^2 (1/3 + u/5),  u = d^2/s^2
+//   log branch:     num = d,      den = (ln y - ln x)/2        (per-node logs)
+// i.e. s / (1 + u/3 + u^2/5) scaled by s^2, so u is only needed inside the
+// correction, where the raw MUFU reciprocal (rel. err ~2^-22) costs < 1e-16.
+// Branch test: integer comparison of the IEEE high words of d^2 and s^2,
+// series iff hi(d^2) - hi(s^2) < -(hi(1.0) - hi(1e-5)), i.e. u below ~1e-5 -
+// the test of the oracle (oracle/euler_oracle.py:series_branch, euler_oracle.c)
+// verbatim, on the ALU (no FP64 compare).  Under it the truncated u^3/7 term is
+// < 2e-16 relative; above it the per-node log difference loses at most
+// ~|ln x| 1e-16 / (2|d/s|), |d/s| >= 3e-3 -> < 4e-14 relative.  The final
+// division happens in the caller's combined reciprocal.
 __device__ __forceinline__ void logmean_parts(double hx, double hy, double hlx, double hly,
                                               double& num, double& den) {
   const double d = __dsub_rn(hy, hx);
   const double s = __dadd_rn(hx, hy);
   const double d2 = __dmul_rn(d, d);
   const double s2 = __dmul_rn(s, s);
-#if SFB_EXACT_LOGMEAN_TEST
-  const bool series = d2 < __dmul_rn(kLogMeanEps, s2);
-#else
-  // Branch choice on the high words (integer ALU, no FP64 op): d^2/s^2 below
-  // ~2^-13.3 (1e-4 within a factor ~1.5).  Both branches are accurate on the
-  // fuzzy band (series truncation < 4e-16 for u < 2e-4; log branch < 1e-14
-  // for u > 5e-5), so a choice that differs from the oracle's exact test near
-  // the threshold changes the result by < 1e-14 relative.
-  const bool series = (__double2hiint(d2) - __double2hiint(s2)) < -(int)(0x3ff00000 - 0x3f1a36e2);
-#endif
-  const double u = d2 * rcp_approx(s2);
-  const double q = fma(u, fma(u, 1.0 / 7.0, 1.0 / 5.0), 1.0 / 3.0);
-  num = dsel(series, s * s2, d);
-  den = dsel(series, fma(d2, q, s2), __dsub_rn(hly, hlx));
-}
-
-// Leaner log mean for the n = 4 warp kernel (FP64 is its bottleneck): the
-// series branch is taken for u = d^2/s^2 below ~1e-5 (instead of 1e-4), where
-// den = s^2 + d^2 (1/3 + u/5) is exact to the u^3/7 < 1e-15 truncation: one
-// DFMA fewer than the three-term series.  On the log branch the per-node log
-// difference loses at most ~|ln x| 1e-16 / (2|d/s|), |d/s| >= 3e-3 ->
-// < 4e-14 relative between 1e-5 and the oracle's 1e-4 threshold
-// (tests/test_gpu_euler.py::test_log_mean_branch_band_matches_oracle).
-// Measured alternatives that were slower: forming u/5 in FP32 (from the high
-// words, or with cvt) - the FP64 saved does not pay for the extra ALU work.
-__device__ __forceinline__ void logmean_parts_v2(double hx, double hy, double hlx, double hly,
-                                                 double& num, double& den) {
-  const double d = __dsub_rn(hy, hx);
-  const double s = __dadd_rn(hx, hy);
-  const double d2 = __dmul_rn(d, d);
-  const double s2 = __dmul_rn(s, s);
-  // u < ~1e-5 on the high words (hi(1e-5) = 0x3ee4f8b5), integer ALU only
   const bool series = (__double2hiint(d2) - __double2hiint(s2)) < -(int)(0x3ff00000 - 0x3ee4f8b5);
   const double q = fma(d2 * rcp_approx(s2), 0.2, 1.0 / 3.0);
   num = dsel(series, s * s2, d);
@@ -192,8 +196,8 @@ __device__ __forceinline__ void chandrashekar_cart_v2(const NodeRec* const (&A)[
   }
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    logmean_parts_v2(A[k]->hr, B[k]->hr, A[k]->hlr, B[k]->hlr, nr[k], dr[k]);  // rho_ln
-    logmean_parts_v2(A[k]->hb, B[k]->hb, A[k]->hlb, B[k]->hlb, nb[k], db[k]);  // beta_ln/c
+    logmean_parts(A[k]->hr, B[k]->hr, A[k]->hlr, B[k]->hlr, nr[k], dr[k]);  // rho_ln
+    logmean_parts(A[k]->hb, B[k]->hb, A[k]->hlb, B[k]->hlb, nb[k], db[k]);  // beta_ln/c
   }
   double sr[K], sb[K], p1[K], rr[K];
 #pragma unroll

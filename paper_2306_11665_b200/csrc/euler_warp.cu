@@ -26,8 +26,20 @@
 #ifndef SFB_WARP_K
 #define SFB_WARP_K 3
 #endif
+#ifndef SFB_EXP_NO_PREP
+#define SFB_EXP_NO_PREP 0
+#endif
+#ifndef SFB_WARP_LDG
+#define SFB_WARP_LDG 1  // states read straight from HBM/L2 (no smem slot)
+#endif
+#ifndef SFB_EXP_NO_MEM
+#define SFB_EXP_NO_MEM 0
+#endif
+#ifndef SFB_EXP_NO_LINE
+#define SFB_EXP_NO_LINE 0
+#endif
 #ifndef SFB_WARP_MINBLOCKS
-#define SFB_WARP_MINBLOCKS 13
+#define SFB_WARP_MINBLOCKS 12
 #endif
 
 namespace sfb {
@@ -35,7 +47,7 @@ namespace sfb {
 namespace {
 constexpr int kN = 4, kNN = 64, kEPW = 2, kS = kEPW * kNN;  // nodes per warp block
 constexpr int kSlotVals = kEPW * 5 * kNN;
-constexpr int kWarpVals = kSlotVals + 7 * kS + 5 * kS;
+constexpr int kWarpVals = (SFB_WARP_LDG ? 0 : kSlotVals) + 7 * kS + 5 * kS;
 constexpr size_t kWarpSmem = (size_t)kWarpVals * sizeof(double);
 }  // namespace
 
@@ -44,6 +56,11 @@ constexpr size_t kWarpSmem = (size_t)kWarpVals * sizeof(double);
 __device__ __forceinline__ void line_pairs4(const double* __restrict__ rec, const int (&pos)[4],
                                             int vp0, int vp1, int vp2, const DMat<4> Dm,
                                             double gm1, double (&acc)[4][5]) {
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int v = 0; v < 5; ++v) acc[a][v] = 0.0;
+  if (SFB_EXP_NO_LINE) return;  // ablation builds only
   NodeRec nrec[4];
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
@@ -57,10 +74,6 @@ __device__ __forceinline__ void line_pairs4(const double* __restrict__ rec, cons
     nrec[a].hlb = pr[6 * kS];
     nrec[a].q = 0.0;
   }
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int v = 0; v < 5; ++v) acc[a][v] = 0.0;
   constexpr PairOrder<4> po;
   constexpr int P = PairOrder<4>::kPairs;
   constexpr int K = SFB_WARP_K;
@@ -100,7 +113,7 @@ __global__ void __launch_bounds__(32 * SFB_WARP_WPC, SFB_WARP_MINBLOCKS)
   __shared__ double ddiag[4];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* slot = smem + warp * kWarpVals;
-  double* rec = slot + kSlotVals;
+  double* rec = slot + (SFB_WARP_LDG ? 0 : kSlotVals);
   double* res = rec + 7 * S;
   if (threadIdx.x == 0) {  // static indices: a dynamic index would copy Dm to local memory
 #pragma unroll
@@ -129,6 +142,7 @@ __global__ void __launch_bounds__(32 * SFB_WARP_WPC, SFB_WARP_MINBLOCKS)
 
   // this lane's line in each direction: element el, transverse (u, w)
   const int el = lane >> 4, L = lane & 15, u = L & 3, w = L >> 2;
+  const double hgm1 = 0.5 * gm1;
   const double* rl = rec + el * NN;
   double* rs = res + el * NN;
   int pos2[N], pos1[N], pos0[N];
@@ -139,47 +153,78 @@ __global__ void __launch_bounds__(32 * SFB_WARP_WPC, SFB_WARP_MINBLOCKS)
     pos2[a] = swz<N>(u, w, a);
   }
 
-  if (niter > 0 && lane == 0) issue(0);
+  // the D diagonal at this lane's prep nodes (c0, c1 fixed per lane; c2 by j parity)
+  const double dd0 = ddiag[lane & 3], dd1 = ddiag[(lane >> 2) & 3];
+  const double dd2e = ddiag[lane >> 4], dd2o = ddiag[(lane >> 4) + 2];
+  auto prefetch = [&](int it) {
+    const int64_t wb = g + (int64_t)it * G;
+    const uint32_t bytes = (uint32_t)nel_of(wb) * 5 * NN * 8;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(U + wb * kEPW * 5 * NN),
+                 "r"(bytes)
+                 : "memory");
+  };
+
+  if (SFB_WARP_LDG) {
+    if (lane == 0 && niter > 0) prefetch(0);
+    if (lane == 0 && niter > 1) prefetch(1);
+  } else if (niter > 0 && lane == 0) {
+    issue(0);
+  }
   for (int it = 0; it < niter; ++it) {
     const int64_t wb = g + (int64_t)it * G;
     const int nel = nel_of(wb);
-    mbar_wait_parity(&full[warp], it & 1);
+    if (SFB_WARP_LDG) {
+      if (lane == 0 && it + 2 < niter) prefetch(it + 2);
+    } else if (!SFB_EXP_NO_MEM || it == 0) {
+      mbar_wait_parity(&full[warp], it & 1);
+    }
     // ---- node records + diagonal term (4 nodes per lane) ----------------------
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
+      if (SFB_EXP_NO_PREP && it > 0) break;  // ablation builds only
       const int i = lane + 32 * j;
       const int e = i >> 6, r = i & 63;
-      const double* uu = slot + e * 5 * NN + r;
-      const double rho = uu[0], m0 = uu[NN], m1 = uu[2 * NN], m2 = uu[3 * NN], et = uu[4 * NN];
-      const double hirho = 0.5 * rcp_refined(rho);
+      double rho, m0, m1, m2, et;
+      if (SFB_WARP_LDG) {
+        const double* uu = U + (wb * kEPW + (e < nel ? e : 0)) * 5 * NN + r;
+        rho = __ldcs(uu);
+        m0 = __ldcs(uu + NN);
+        m1 = __ldcs(uu + 2 * NN);
+        m2 = __ldcs(uu + 3 * NN);
+        et = __ldcs(uu + 4 * NN);
+      } else {
+        const double* uu = slot + e * 5 * NN + r;
+        rho = uu[0], m0 = uu[NN], m1 = uu[2 * NN], m2 = uu[3 * NN], et = uu[4 * NN];
+      }
+      const double irho = rcp_refined(rho);
+      const double hirho = 0.5 * irho;
       const double mm = fma(m2, m2, fma(m1, m1, m0 * m0));
-      const double X = fma(rho, et, -0.5 * mm);
-      const double iX = rcp_refined(X);
-      const double p = (2.0 * gm1) * X * hirho;
-      const double hbeta = 0.5 * (rho * rho) * iX;  // (gamma - 1) beta
-      const double hr = 0.5 * rho, h0 = m0 * hirho, h1 = m1 * hirho, h2 = m2 * hirho;
+      const double X2 = fma(rho, et + et, -mm);  // 2 (rho E - |m|^2/2)
+      const double iX2 = rcp_refined(X2);
+      const double p = (hgm1 * X2) * irho;
+      const double hbeta = (rho * rho) * iX2;  // (gamma - 1) beta = rho^2 / (2X)
       const int c0 = r & 3, c1 = (r >> 2) & 3, c2 = r >> 4;
       const int q = e * NN + swz<N>(c0, c1, c2);
-      rec[q] = hr;
-      rec[S + q] = h0;
-      rec[2 * S + q] = h1;
-      rec[3 * S + q] = h2;
+      rec[q] = 0.5 * rho;
+      rec[S + q] = m0 * hirho;
+      rec[2 * S + q] = m1 * hirho;
+      rec[3 * S + q] = m2 * hirho;
       rec[4 * S + q] = hbeta;
-      rec[5 * S + q] = log_half(rho);
-      rec[6 * S + q] = log_half(hbeta);
-      const double hq = fma(h2, h2, fma(h1, h1, h0 * h0));
-      const double d0 = ddiag[c0], d1 = ddiag[c1], d2 = ddiag[c2];
-      const double wv = 2.0 * fma(d2, h2, fma(d1, h1, d0 * h0));
-      const double rw = 2.0 * hr * wv;
-      const double ep = fma(gam_ratio, p, 4.0 * hr * hq);
-      res[q] = rw;
-      res[S + q] = fma(2.0 * rw, h0, p * d0);
-      res[2 * S + q] = fma(2.0 * rw, h1, p * d1);
-      res[3 * S + q] = fma(2.0 * rw, h2, p * d2);
-      res[4 * S + q] = ep * wv;
+      rec[5 * S + q] = log_half_tab(rho);
+      rec[6 * S + q] = log_half_tab(hbeta);
+      // diagonal term sum_j D_{c_j c_j} f_j(u, u): with mass = D.m and
+      // w = mass / rho:  (mass, w m + p D, (E + p) w)
+      const double d0 = dd0, d1 = dd1, d2 = (j & 1) ? dd2o : dd2e;
+      const double mass = fma(d2, m2, fma(d1, m1, d0 * m0));
+      const double wv = mass * irho;
+      res[q] = mass;
+      res[S + q] = fma(wv, m0, p * d0);
+      res[2 * S + q] = fma(wv, m1, p * d1);
+      res[3 * S + q] = fma(wv, m2, p * d2);
+      res[4 * S + q] = (et + p) * wv;
     }
     __syncwarp();
-    if (lane == 0 && it + 1 < niter) {  // the slot is consumed: refill it
+    if (!SFB_WARP_LDG && !SFB_EXP_NO_MEM && lane == 0 && it + 1 < niter) {  // slot consumed: refill
       fence_proxy_async_smem();
       issue(it + 1);
     }
@@ -209,7 +254,7 @@ __global__ void __launch_bounds__(32 * SFB_WARP_WPC, SFB_WARP_MINBLOCKS)
     // ---- lines along x0: finish and store (4 contiguous doubles per variable) --
     line_pairs4(rl, pos0, 1 * S, 2 * S, 3 * S, Dm, gm1, acc);
     __syncwarp();
-    if (el < nel) {
+    if (SFB_EXP_NO_MEM ? (nel == 12345) : (el < nel)) {
       double* out = R + (wb * kEPW + el) * 5 * NN + 4 * L;
 #pragma unroll
       for (int v = 0; v < 5; ++v) {

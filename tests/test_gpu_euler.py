@@ -166,7 +166,7 @@ def test_many_blocks_per_cta_odd_sizes(n):
 def test_log_mean_branch_band_matches_oracle():
     # element-wise perturbations of a constant state with amplitudes 1e-1..1e-7:
     # neighbour ratios sweep u = (d/s)^2 through both log-mean branches and
-    # the band between the kernel's and the oracle's thresholds (1e-5 / 1e-4)
+    # across the ~1e-5 threshold
     n, E = 4, 512
     U = eu.generate_states(E, n, seed=21)
     base = U[:, :, :1].clone()
