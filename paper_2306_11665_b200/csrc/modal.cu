@@ -20,9 +20,11 @@
 //            diagonal term sum_i D[r_i,r_i] F#(u_r,u_r; Ja^i(r)) into the
 //            residual (consistency: F#(u,u;n) = f(u).n);
 //   stage C  thread per (direction, line): each symmetric pair once, scattered
-//            to both rows; direction-ordered accumulation (3 barrier phases);
-//   stage D  three passes of Pi; Rhat streamed out; per-thread squares summed
-//            in a fixed order, then a fixed smem tree -> sumsq[e].
+//            to both rows; each direction's residual into its own buffer (one
+//            barrier; the x0 buffer reuses the slot's free Uhat region);
+//   stage D  three passes of Pi, the first summing diagonal + 3 direction
+//            buffers on the fly; Rhat streamed out; per-thread squares summed
+//            in a fixed order, xor-butterfly per warp, warps in order -> sumsq[e].
 // The metric averaging 1/2 is folded into D (Ft is linear in n).
 #include "bulk.cuh"
 #include "common.cuh"
@@ -55,16 +57,21 @@ struct ModalCfg {
   static constexpr int kU = 5 * kNodes;   // doubles of Uhat / u / r per element
   static constexpr int kJ = 9 * kNodes;   // doubles of Ja per element
   static constexpr int kSlot = kU + kJ;   // one input slot
-  static constexpr int kRec = 8 * kNodes; // node records: 7 planes + p
-  static constexpr int kRedPow2 = kThreads <= 128 ? 128 : (kThreads <= 256 ? 256 : 512);
+  static constexpr int kRec = 7 * kNodes; // node records: 7 planes
   static constexpr size_t kSmem =
-      (size_t)(2 * kSlot + kRec + kU /*residual*/ + kRedPow2) * sizeof(double);
+      (size_t)(2 * kSlot + kRec + 3 * kU /*residual + 2 direction buffers*/) * sizeof(double);
   static constexpr int kMinBlocks = (N == 6) ? SFB_MODAL_MINBLOCKS_N6 : 1;
 };
 
-// one sum-factorised pass along direction j: out[.., a_j, ..] = sum_c A[a_j][c] in[.., c, ..]
+// One sum-factorised pass along direction j:
+//   out[.., a_j, ..] = sum_c A[a_j][c] in[.., c, ..]
+// A is a reference into the __grid_constant__ parameter block, so with the
+// loops unrolled every coefficient is a constant-bank operand of its DFMA (no
+// shared-memory load per multiply: 56 -> 52.5 ms at config 5).  One work item
+// per (variable, line); splitting a line's outputs over two items to fill the
+// CTA more evenly measured slower (58.8 ms: the inputs are loaded twice).
 template <int N>
-__device__ __forceinline__ void kron_pass(const double* __restrict__ A, int j,
+__device__ __forceinline__ void kron_pass(const double (&A)[N * N], int j,
                                           const double* __restrict__ in, double* __restrict__ out,
                                           int tid, int nthreads) {
   constexpr int NN = N * N * N;
@@ -92,13 +99,51 @@ __device__ __forceinline__ void kron_pass(const double* __restrict__ A, int j,
   }
 }
 
+// kron_pass whose input is the sum of four buffers, ((a + b) + c) + d at each
+// node (diagonal term + the three direction residuals, in that order).  Each
+// line is read completely before it is written, and lines are disjoint, so
+// out may alias any input.
+template <int N>
+__device__ __forceinline__ void kron_pass_sum4(const double (&A)[N * N], int j,
+                                               const double* in0, const double* in1,
+                                               const double* in2, const double* in3, double* out,
+                                               int tid, int nthreads) {
+  constexpr int NN = N * N * N;
+  const int stride = j == 0 ? 1 : (j == 1 ? N : N * N);
+  for (int t = tid; t < 5 * N * N; t += nthreads) {
+    const int v = t / (N * N);
+    const int L = t - v * N * N;
+    const int u0 = L % N, u1 = L / N;
+    int base;
+    if (j == 0) base = u0 * N + u1 * N * N;
+    else if (j == 1) base = u0 + u1 * N * N;
+    else base = u0 + u1 * N;
+    const int o = v * NN + base;
+    double x[N];
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      const int k = o + c * stride;
+      x[c] = ((in0[k] + in1[k]) + in2[k]) + in3[k];
+    }
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+      double acc = 0.0;
+#pragma unroll
+      for (int c = 0; c < N; ++c) acc = fma(A[a * N + c], x[c], acc);
+      out[o + a * stride] = acc;
+    }
+  }
+}
+
 // Contravariant Chandrashekar flux for K pairs at once (normals n = Ja_a + Ja_b,
-// the 1/2 being folded into D).
+// the 1/2 being folded into D).  Records carry hb = (gamma-1) beta (see
+// chandrashekar_cart_v2 in euler_flux.cuh): the beta log mean's reciprocal is
+// then c_gamma / beta_ln directly and p_hat = gm1 rhobar / sb.
 template <int K>
 __device__ __forceinline__ void chandrashekar_curv_k(const NodeRec (&A)[K],
                                                      const NodeRec (&B)[K],
                                                      const double (&nx)[K], const double (&ny)[K],
-                                                     const double (&nz)[K], double c_gamma,
+                                                     const double (&nz)[K], double gm1,
                                                      double (&f)[K][5]) {
   double vb0[K], vb1[K], vb2[K], nr[K], dr[K], nb[K], db[K];
 #pragma unroll
@@ -118,8 +163,8 @@ __device__ __forceinline__ void chandrashekar_curv_k(const NodeRec (&A)[K],
     const double inv_sb = rr * p1;
     const double t = rr * sb;
     const double rho_ln = nr[k] * (t * nb[k]);
-    const double ibeta = db[k] * (t * dr[k]);
-    const double phat = 0.5 * sr * inv_sb;
+    const double cibeta = db[k] * (t * dr[k]);  // c_gamma / beta_ln
+    const double phat = (gm1 * sr) * inv_sb;
     const double vn = fma(vb2[k], nz[k], fma(vb1[k], ny[k], vb0[k] * nx[k]));
     const double f1 = rho_ln * vn;
     f[k][0] = f1;
@@ -127,8 +172,7 @@ __device__ __forceinline__ void chandrashekar_curv_k(const NodeRec (&A)[K],
     f[k][2] = fma(f1, vb1[k], phat * ny[k]);
     f[k][3] = fma(f1, vb2[k], phat * nz[k]);
     const double dot = fma(A[k].hv2, B[k].hv2, fma(A[k].hv1, B[k].hv1, A[k].hv0 * B[k].hv0));
-    const double g = fma(2.0, dot, c_gamma * ibeta);
-    f[k][4] = fma(f1, g, phat * vn);
+    f[k][4] = fma(f1, fma(2.0, dot, cibeta), phat * vn);
   }
 }
 
@@ -157,7 +201,7 @@ constexpr int kModalBatch = (N >= 7) ? 1 : (N == 6 ? SFB_MODAL_BATCH_N6 : (N >= 
 
 template <int N>
 __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks)
-    euler_modal_kernel(int64_t E, const ModalOps<N> ops, double gm1, double c_gamma,
+    euler_modal_kernel(int64_t E, const __grid_constant__ ModalOps<N> ops, double gm1, double c_gamma,
                        double gam_ratio, const double* __restrict__ Uhat,
                        const double* __restrict__ Ja, double* __restrict__ Rhat,
                        double* __restrict__ sumsq) {
@@ -169,30 +213,23 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
   // region doubles as the transform ping-pong buffer: V^3 runs slot -> res ->
   // slot -> res (u ends in res), Pi^3 runs res -> slot -> res -> slot.
   double* slots = smem;                    // [2][Uhat | Ja]
-  double* rec = smem + 2 * Cfg::kSlot;     // [8][NN] node records (natural layout)
+  double* rec = smem + 2 * Cfg::kSlot;     // [7][NN] node records (natural layout)
   double* res = rec + Cfg::kRec;           // [5][NN] u, then the nodal residual r
-  double* red = res + Cfg::kU;             // [T] reduction scratch
+  double* dbuf1 = res + Cfg::kU;           // [5][NN] x1-line residuals
+  double* dbuf2 = dbuf1 + Cfg::kU;         // [5][NN] x2-line residuals
+  __shared__ double wsum[T / 32];
   __shared__ uint64_t full[2];
-  __shared__ double sops[3 * N * N + N];
   const int tid = threadIdx.x;
-  if (tid == 0) {  // static indices only: the parameter block is never copied to local memory
-#pragma unroll
-    for (int i = 0; i < N * N; ++i) {
-      sops[i] = ops.D[i];
-      sops[N * N + i] = ops.V[i];
-      sops[2 * N * N + i] = ops.P[i];
-    }
-#pragma unroll
-    for (int i = 0; i < N; ++i) sops[3 * N * N + i] = ops.Dd[i];
+  const double hgm1 = 0.5 * gm1;
+  if (tid == 0) {
     mbar_init(&full[0], 1);
     mbar_init(&full[1], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  const double* sD = sops;
-  const double* sV = sops + N * N;
-  const double* sP = sops + 2 * N * N;
-  const double* sDd = sops + 3 * N * N;
+  // operators straight from the __grid_constant__ parameter block (constant bank)
+  const double(&sV)[N * N] = ops.V;
+  const double(&sP)[N * N] = ops.P;
 
   constexpr uint32_t kUB = (uint32_t)(Cfg::kU * 8), kJB = (uint32_t)(Cfg::kJ * 8);
   constexpr bool kBulk = (kUB % 16) == 0 && (kJB % 16) == 0;
@@ -237,32 +274,35 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
       const double* u = res + r;  // read this node's u, then overwrite it with its diagonal term
       const double rho = u[0], m0 = u[NN], m1 = u[2 * NN], m2 = u[3 * NN], et = u[4 * NN];
       const double irho = rcp_refined(rho);
-      const double v0 = m0 * irho, v1 = m1 * irho, v2 = m2 * irho;
-      const double vv = fma(v2, v2, fma(v1, v1, v0 * v0));
-      const double p = gm1 * fma(-0.5 * rho, vv, et);
-      const double beta = 0.5 * rho * rcp_refined(p);
+      const double hirho = 0.5 * irho;
+      const double mm = fma(m2, m2, fma(m1, m1, m0 * m0));
+      const double X2 = fma(rho, et + et, -mm);  // 2 (rho E - |m|^2/2)
+      const double iX2 = rcp_refined(X2);
+      const double p = (hgm1 * X2) * irho;
+      const double hbeta = (rho * rho) * iX2;  // (gamma - 1) beta
       rec[r] = 0.5 * rho;
-      rec[NN + r] = 0.5 * v0;
-      rec[2 * NN + r] = 0.5 * v1;
-      rec[3 * NN + r] = 0.5 * v2;
-      rec[4 * NN + r] = 0.5 * beta;
-      rec[5 * NN + r] = 0.5 * log_pos(rho);
-      rec[6 * NN + r] = 0.5 * log_pos(beta);
-      rec[7 * NN + r] = p;
-      // n_diag = sum_i D[r_i,r_i] Ja^i(r)
+      rec[NN + r] = m0 * hirho;
+      rec[2 * NN + r] = m1 * hirho;
+      rec[3 * NN + r] = m2 * hirho;
+      rec[4 * NN + r] = hbeta;
+      rec[5 * NN + r] = log_half_tab(rho);
+      rec[6 * NN + r] = log_half_tab(hbeta);
+      // n_diag = sum_i D[r_i,r_i] Ja^i(r); diagonal term f(u).n_diag with
+      // mass = m.n_diag, w = mass / rho:  (mass, w m + p n_diag, (E + p) w)
       const int c0 = r % N, c1 = (r / N) % N, c2 = r / (N * N);
-      const double d0 = sDd[c0], d1 = sDd[c1], d2 = sDd[c2];
+      const double d0 = ops.Dd[c0], d1 = ops.Dd[c1], d2 = ops.Dd[c2];
       double nd[3];
 #pragma unroll
       for (int m = 0; m < 3; ++m)
         nd[m] = fma(d2, jin[(2 * 3 + m) * NN + r],
                     fma(d1, jin[(1 * 3 + m) * NN + r], d0 * jin[(0 * 3 + m) * NN + r]));
-      const double vn = fma(v2, nd[2], fma(v1, nd[1], v0 * nd[0]));
-      res[r] = rho * vn;
-      res[NN + r] = fma(m0, vn, p * nd[0]);
-      res[2 * NN + r] = fma(m1, vn, p * nd[1]);
-      res[3 * NN + r] = fma(m2, vn, p * nd[2]);
-      res[4 * NN + r] = fma(gam_ratio * p, vn, 0.5 * rho * vv * vn);  // (E + p) vn
+      const double mass = fma(m2, nd[2], fma(m1, nd[1], m0 * nd[0]));
+      const double wv = mass * irho;
+      res[r] = mass;
+      res[NN + r] = fma(m0, wv, p * nd[0]);
+      res[2 * NN + r] = fma(m1, wv, p * nd[1]);
+      res[3 * NN + r] = fma(m2, wv, p * nd[2]);
+      res[4 * NN + r] = (et + p) * wv;
     }
     __syncthreads();
 
@@ -315,12 +355,12 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
             nz[k] = jd[2 * NN + ka] + jd[2 * NN + kb];
           }
           double f[K][5];
-          chandrashekar_curv_k<K>(A, B, nx, ny, nz, c_gamma, f);
+          chandrashekar_curv_k<K>(A, B, nx, ny, nz, gm1, f);
 #pragma unroll
           for (int k = 0; k < K; ++k) {
             if (k0 + k >= P) break;
             const int a = po.a[k0 + k], b = po.b[k0 + k];
-            const double dab = sD[a * N + b], dba = sD[b * N + a];
+            const double dab = ops.D[a * N + b], dba = ops.D[b * N + a];
 #pragma unroll
             for (int v = 0; v < 5; ++v) {
               acc[a][v] = fma(dab, f[k][v], acc[a][v]);
@@ -329,42 +369,41 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
           }
         }
       }
+      if (active) {  // every node is on exactly one line per direction: plain stores
+        double* db = dir == 0 ? in : (dir == 1 ? dbuf1 : dbuf2);
 #pragma unroll
-      for (int phase = 0; phase < 3; ++phase) {
-        if (active && dir == phase) {
+        for (int a = 0; a < N; ++a)
 #pragma unroll
-          for (int a = 0; a < N; ++a)
-#pragma unroll
-            for (int v = 0; v < 5; ++v) res[v * NN + base + a * stride] += acc[a][v];
-        }
-        __syncthreads();
+          for (int v = 0; v < 5; ++v) db[v * NN + base + a * stride] = acc[a][v];
       }
+      __syncthreads();
     }
 
     // ---- stage D: Rhat = Pi^3 r, store, sum of squares -------------------------
-    kron_pass<N>(sP, 0, res, in, tid, T);
+    kron_pass_sum4<N>(sP, 0, res, in, dbuf1, dbuf2, res, tid, T);  // r = diag + x0 + x1 + x2
     __syncthreads();
-    kron_pass<N>(sP, 1, in, res, tid, T);
+    kron_pass<N>(sP, 1, res, in, tid, T);
     __syncthreads();
-    kron_pass<N>(sP, 2, res, in, tid, T);  // Rhat in the slot's Uhat region
+    kron_pass<N>(sP, 2, in, res, tid, T);  // Rhat in res
     __syncthreads();
     double* Rg = Rhat + e * Cfg::kU;
     double ss = 0.0;
     for (int i = tid; i < Cfg::kU; i += T) {
-      const double x = in[i];
+      const double x = res[i];
       __stcs(Rg + i, x);
       ss = fma(x, x, ss);
     }
-    if (sumsq) {  // fixed-shape tree over a power-of-two padded array
-      constexpr int RP = Cfg::kRedPow2;
-      red[tid] = ss;
-      for (int i = T + tid; i < RP; i += T) red[i] = 0.0;
+    if (sumsq) {  // fixed order: xor-butterfly in each warp, then the warps in order
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if ((tid & 31) == 0) wsum[tid >> 5] = ss;
       __syncthreads();
-      for (int w = RP / 2; w >= 1; w /= 2) {
-        for (int i = tid; i < w; i += T) red[i] = red[i] + red[i + w];
-        __syncthreads();
+      if (tid == 0) {
+        double t = wsum[0];
+#pragma unroll
+        for (int w = 1; w < T / 32; ++w) t += wsum[w];
+        sumsq[e] = t;
       }
-      if (tid == 0) sumsq[e] = red[0];
     }
     __syncthreads();
   }
