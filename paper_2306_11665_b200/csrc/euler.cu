@@ -49,6 +49,9 @@
 #ifndef SFB_WARP_N4
 #define SFB_WARP_N4 1  // warp-autonomous kernel (euler_warp.cu)
 #endif
+#ifndef SFB_WARP_SMALL
+#define SFB_WARP_SMALL 1  // 1: n = 2 on the warp-autonomous kernel; 2: n = 3, 5 too
+#endif
 #ifndef SFB_FUSED_N4
 #define SFB_FUSED_N4 1
 #endif
@@ -403,20 +406,27 @@ int launch_euler_cart4_split(int64_t E, const double* Dh, double gamma, double s
 int launch_euler_cart4_fused(int64_t E, const double* Dh, double gamma, double scale,
                              const double* U, double* R, cudaStream_t s);
 
-int launch_euler_cart4_warp(int64_t E, const double* Dh, double gamma, double scale,
-                            const double* U, double* R, cudaStream_t s);
+template <int N>
+int launch_euler_cart_warp(int64_t E, const double* Dh, double gamma, double scale,
+                           const double* U, double* R, cudaStream_t s);
 
 int euler_cartesian_dispatch(int64_t E, int64_t n, const double* D_host, double gamma,
                              double scale, const double* U, double* R, cudaStream_t s) {
   switch (n) {
-    case 2: return launch_euler_cartesian<2>(E, D_host, gamma, scale, U, R, s);
-    case 3: return launch_euler_cartesian<3>(E, D_host, gamma, scale, U, R, s);
+    case 2:
+      return SFB_WARP_SMALL ? launch_euler_cart_warp<2>(E, D_host, gamma, scale, U, R, s)
+                            : launch_euler_cartesian<2>(E, D_host, gamma, scale, U, R, s);
+    case 3:  // warp kernel measured 0.673 vs 0.657 ms (config 4): CTA kernel
+      return SFB_WARP_SMALL > 1 ? launch_euler_cart_warp<3>(E, D_host, gamma, scale, U, R, s)
+                                : launch_euler_cartesian<3>(E, D_host, gamma, scale, U, R, s);
     case 4:
-      if (SFB_WARP_N4) return launch_euler_cart4_warp(E, D_host, gamma, scale, U, R, s);
+      if (SFB_WARP_N4) return launch_euler_cart_warp<4>(E, D_host, gamma, scale, U, R, s);
       if (SFB_FUSED_N4) return launch_euler_cart4_fused(E, D_host, gamma, scale, U, R, s);
       return SFB_SPLIT_N4 ? launch_euler_cart4_split(E, D_host, gamma, scale, U, R, s)
                           : launch_euler_cartesian<4>(E, D_host, gamma, scale, U, R, s);
-    case 5: return launch_euler_cartesian<5>(E, D_host, gamma, scale, U, R, s);
+    case 5:  // warp kernel (25 of 32 lanes) measured 1.02 vs 0.85 ms: CTA kernel
+      return SFB_WARP_SMALL > 1 ? launch_euler_cart_warp<5>(E, D_host, gamma, scale, U, R, s)
+                                : launch_euler_cartesian<5>(E, D_host, gamma, scale, U, R, s);
     case 6: return launch_euler_cartesian<6>(E, D_host, gamma, scale, U, R, s);
     case 7: return launch_euler_cartesian<7>(E, D_host, gamma, scale, U, R, s);
     case 8: return launch_euler_cartesian<8>(E, D_host, gamma, scale, U, R, s);
