@@ -123,10 +123,33 @@ int sfb_hadamard_rowsum_batched(int64_t E, int64_t m, int64_t n, int64_t d, cons
  * out[e,r] = -(2/omega_r) sum_j sum_k Q_j[r,k] f(u_r, u_k), evaluated as
  * -(2/omega_r) * sum_j (hadamard row sum of direction j); qfactors is the
  * assembled (d, n^d, n) basis factor set of Q = W D (burgers.py:87-97),
- * inv_omega (n^d) = 1/omega.  u (E, n^d) -> out (E, n^d). */
+ * omega (n^d) the tensor-product weights.  u (E, n^d) -> out (E, n^d). */
 int sfb_burgers_volume(int64_t E, int64_t n, int64_t d, const double* qfactors,
                        const double* omega, int flux, const double* u, double* out,
                        sfb_stream_t stream);
+
+/* ---- periodic Burgers time derivative (burgers.py:134-162) -------------
+ * dudt = volume term (as sfb_burgers_volume) + the periodic interface term of
+ * _surface_residual (burgers.py:134-156): per direction, in order, right-face
+ * nodes -= (f*(u_R,u_L) - u_R^2/2)/w[n-1], left-face nodes
+ * += (f*(u_R,u_L) - u_L^2/2)/w[0]; w0 = w[0], wn = w[n-1] of the GLL rule.
+ * Bitwise equal to the reference's time_derivative.  flux: BURGERS_EC/AVG. */
+int sfb_burgers_time_derivative(int64_t E, int64_t n, int64_t d, const double* qfactors,
+                                const double* omega, double w0, double wn, int flux,
+                                const double* u, double* dudt, sfb_stream_t stream);
+
+/* ---- RK4 time integration of a batch of periodic Burgers elements ------
+ * (demos/burgers_entropy.py:25-33, classic RK4 on time_derivative), `steps`
+ * steps of size dt, all in ONE launch (one CTA per element, n^d <= 1024);
+ * u (E, n^d) is advanced in place, bitwise equal to the reference's
+ * trajectory.  Monitors every `every` steps, before the step (step 0, every,
+ * ..., incl. `steps` when divisible): entropy[e, k] = 0.5 sum_r omega_r u_r^2
+ * (burgers.py:165-169) and mass[e, k] = sum_r omega_r u_r, each
+ * (E, steps/every + 1), fixed-order sums; either may be NULL (every = 0: no
+ * monitors). */
+int sfb_burgers_rk4(int64_t E, int64_t n, int64_t d, const double* qfactors, const double* omega,
+                    double w0, double wn, int flux, double dt, int64_t steps, int64_t every,
+                    double* u, double* entropy, double* mass, sfb_stream_t stream);
 
 /* ---- sum-factorized Kronecker apply (operators.py:274-318) -------------
  * y[b] = (A_{d-1} x ... x A_0) x[b] for a batch of B vectors; factors is a

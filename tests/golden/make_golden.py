@@ -206,10 +206,47 @@ def make_burgers(sf):
         out[f"vol_ec_{d}_{n}"] = sf.volume_residual(st)
         out[f"vol_avg_{d}_{n}"] = sf.volume_residual(st, sf.average_flux)
         out[f"dudt_{d}_{n}"] = sf.time_derivative(st)
+        out[f"dudt_avg_{d}_{n}"] = sf.time_derivative(st, sf.average_flux)
         out[f"dsdt_{d}_{n}"] = np.array(sf.entropy_time_derivative(st))
         out[f"dsdt_avg_{d}_{n}"] = np.array(sf.entropy_time_derivative(st, sf.average_flux))
         out[f"entropy_{d}_{n}"] = np.array(sf.total_entropy(st))
     np.savez_compressed(os.path.join(HERE, "burgers.npz"), **out)
+
+
+def reference_rk4(sf, d, n, u, dt, steps, flux, every):
+    """demos/burgers_entropy.py:25-51 verbatim in structure: classic RK4 on the
+    reference's time_derivative, entropy sampled before every `every` steps."""
+
+    def rhs(v):
+        return sf.time_derivative(sf.BurgersState(d, n, v), flux)
+
+    trace = []
+    for step in range(steps + 1):
+        if step % every == 0:
+            trace.append(sf.total_entropy(sf.BurgersState(d, n, u)))
+        if step == steps:
+            break
+        k1 = rhs(u)
+        k2 = rhs(u + 0.5 * dt * k1)
+        k3 = rhs(u + 0.5 * dt * k2)
+        k4 = rhs(u + dt * k3)
+        u = u + dt / 6.0 * (k1 + 2 * k2 + 2 * k3 + k4)
+    return u, np.array(trace)
+
+
+RK4_CASES = [(2, 5, 2e-3, 40, 10), (1, 6, 1e-3, 30, 10), (3, 4, 2e-3, 12, 4)]
+
+
+def make_burgers_rk4(sf):
+    out = {}
+    for d, n, dt, steps, every in RK4_CASES:
+        u0 = synth.uniform_array(n**d, 300 + 10 * d + n, -1.0, 1.0)
+        out[f"u0_{d}_{n}"] = u0
+        for name, flux in (("ec", sf.ec_two_point_flux), ("avg", sf.average_flux)):
+            u, trace = reference_rk4(sf, d, n, u0.copy(), dt, steps, flux, every)
+            out[f"u_{name}_{d}_{n}"] = u
+            out[f"entropy_{name}_{d}_{n}"] = trace
+    np.savez_compressed(os.path.join(HERE, "burgers_rk4.npz"), **out)
 
 
 def make_kron(sf):
@@ -299,6 +336,7 @@ def main():
     make_config2(sf)
     make_euler(sf)
     make_burgers(sf)
+    make_burgers_rk4(sf)
     make_kron(sf)
     make_modal(sf)
     print("golden fixtures written to", HERE)
