@@ -33,6 +33,9 @@
 #ifndef SFB_MODAL_MINBLOCKS_N6
 #define SFB_MODAL_MINBLOCKS_N6 2
 #endif
+#ifndef SFB_MODAL_COMPACT
+#define SFB_MODAL_COMPACT 0  // 1: 69 KB smem but one more barrier: 51.0 vs 47.9 ms
+#endif
 #ifndef SFB_MODAL_BATCH_N6
 #define SFB_MODAL_BATCH_N6 3
 #endif
@@ -58,8 +61,10 @@ struct ModalCfg {
   static constexpr int kJ = 9 * kNodes;   // doubles of Ja per element
   static constexpr int kSlot = kU + kJ;   // one input slot
   static constexpr int kRec = 7 * kNodes; // node records: 7 planes
+  // residual (+ 2 direction buffers unless SFB_MODAL_COMPACT reuses the
+  // record planes and the residual itself for them)
   static constexpr size_t kSmem =
-      (size_t)(2 * kSlot + kRec + 3 * kU /*residual + 2 direction buffers*/) * sizeof(double);
+      (size_t)(2 * kSlot + kRec + (SFB_MODAL_COMPACT ? 1 : 3) * kU) * sizeof(double);
   static constexpr int kMinBlocks = (N == 6) ? SFB_MODAL_MINBLOCKS_N6 : 1;
 };
 
@@ -99,12 +104,12 @@ __device__ __forceinline__ void kron_pass(const double (&A)[N * N], int j,
   }
 }
 
-// kron_pass whose input is the sum of four buffers, ((a + b) + c) + d at each
-// node (diagonal term + the three direction residuals, in that order).  Each
+// kron_pass whose input is the sum of NIN (3 or 4) buffers, ((a + b) + c) + d
+// at each node (diagonal term + the direction residuals).  Each
 // line is read completely before it is written, and lines are disjoint, so
 // out may alias any input.
-template <int N>
-__device__ __forceinline__ void kron_pass_sum4(const double (&A)[N * N], int j,
+template <int N, int NIN>
+__device__ __forceinline__ void kron_pass_sum(const double (&A)[N * N], int j,
                                                const double* in0, const double* in1,
                                                const double* in2, const double* in3, double* out,
                                                int tid, int nthreads) {
@@ -123,7 +128,8 @@ __device__ __forceinline__ void kron_pass_sum4(const double (&A)[N * N], int j,
 #pragma unroll
     for (int c = 0; c < N; ++c) {
       const int k = o + c * stride;
-      x[c] = ((in0[k] + in1[k]) + in2[k]) + in3[k];
+      x[c] = (in0[k] + in1[k]) + in2[k];
+      if (NIN == 4) x[c] = x[c] + in3[k];
     }
 #pragma unroll
     for (int a = 0; a < N; ++a) {
@@ -215,8 +221,12 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
   double* slots = smem;                    // [2][Uhat | Ja]
   double* rec = smem + 2 * Cfg::kSlot;     // [7][NN] node records (natural layout)
   double* res = rec + Cfg::kRec;           // [5][NN] u, then the nodal residual r
-  double* dbuf1 = res + Cfg::kU;           // [5][NN] x1-line residuals
-  double* dbuf2 = dbuf1 + Cfg::kU;         // [5][NN] x2-line residuals
+  // x1-line residuals: the record planes once every line has read them
+  // (compact), else a buffer of their own; x2-line residuals: added into the
+  // residual in place (compact; each node is on exactly one x2 line), else a
+  // buffer of their own
+  double* dbuf1 = SFB_MODAL_COMPACT ? rec : res + Cfg::kU;
+  double* dbuf2 = SFB_MODAL_COMPACT ? nullptr : res + 2 * Cfg::kU;
   __shared__ double wsum[T / 32];
   __shared__ uint64_t full[2];
   const int tid = threadIdx.x;
@@ -369,18 +379,29 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
           }
         }
       }
+      if (SFB_MODAL_COMPACT) __syncthreads();  // all lines have read the records
       if (active) {  // every node is on exactly one line per direction: plain stores
-        double* db = dir == 0 ? in : (dir == 1 ? dbuf1 : dbuf2);
+        if (SFB_MODAL_COMPACT && dir == 2) {
 #pragma unroll
-        for (int a = 0; a < N; ++a)
+          for (int a = 0; a < N; ++a)
 #pragma unroll
-          for (int v = 0; v < 5; ++v) db[v * NN + base + a * stride] = acc[a][v];
+            for (int v = 0; v < 5; ++v) res[v * NN + base + a * stride] += acc[a][v];
+        } else {
+          double* db = dir == 0 ? in : (dir == 1 ? dbuf1 : dbuf2);
+#pragma unroll
+          for (int a = 0; a < N; ++a)
+#pragma unroll
+            for (int v = 0; v < 5; ++v) db[v * NN + base + a * stride] = acc[a][v];
+        }
       }
       __syncthreads();
     }
 
     // ---- stage D: Rhat = Pi^3 r, store, sum of squares -------------------------
-    kron_pass_sum4<N>(sP, 0, res, in, dbuf1, dbuf2, res, tid, T);  // r = diag + x0 + x1 + x2
+    if (SFB_MODAL_COMPACT)  // r = (diag + x2) + x0 + x1
+      kron_pass_sum<N, 3>(sP, 0, res, in, dbuf1, nullptr, res, tid, T);
+    else  // r = diag + x0 + x1 + x2
+      kron_pass_sum<N, 4>(sP, 0, res, in, dbuf1, dbuf2, res, tid, T);
     __syncthreads();
     kron_pass<N>(sP, 1, res, in, tid, T);
     __syncthreads();
