@@ -49,6 +49,12 @@
 #ifndef SFB_WARP_N4
 #define SFB_WARP_N4 1  // warp-autonomous kernel (euler_warp.cu)
 #endif
+#ifndef SFB_GENERIC_TABLOG
+#define SFB_GENERIC_TABLOG 0  // table log: +30% at n=6 (the single prep warp is latency-bound)
+#endif
+#ifndef SFB_MINBLOCKS_N7
+#define SFB_MINBLOCKS_N7 1  // 2 caps at 168 regs and spills (1.86 vs 1.54 ms at config 4)
+#endif
 #ifndef SFB_WARP_SMALL
 #define SFB_WARP_SMALL 1  // 1: n = 2 on the warp-autonomous kernel; 2: n = 3, 5 too
 #endif
@@ -80,7 +86,8 @@ struct EulerCartCfg {
   // prep warps balance node preprocessing + stores against the line work
   static constexpr int kPrepWarps = (N <= 3) ? 3 : (N == 4 ? SFB_PREP_WARPS_N4 : 1);
   static constexpr int kThreads = 32 * (kLineWarps + kPrepWarps);
-  static constexpr int kMinBlocks = (N == 4) ? SFB_MINBLOCKS_N4 : ((N == 5 || N == 3 || N == 7) ? 2 : 1);
+  static constexpr int kMinBlocks =
+      (N == 4) ? SFB_MINBLOCKS_N4 : (N == 7 ? SFB_MINBLOCKS_N7 : ((N == 5 || N == 3) ? 2 : 1));
   static constexpr int kVals = kEPB * 5 * kNodes;  // doubles per block of states
   static constexpr int kPlanes = 8;                // 7 record planes + pressure
   static constexpr int kRecVals = kPlanes * kEPB * kNodes;
@@ -103,7 +110,7 @@ struct LineOut {
 
 template <int N>
 __device__ __forceinline__ void line_work(const double* __restrict__ rec, int el, int dir, int L,
-                                          const DMat<N>& Dm, double c_gamma, LineOut<N>& o) {
+                                          const DMat<N>& Dm, double gm1, LineOut<N>& o) {
   using Cfg = EulerCartCfg<N>;
   constexpr int NN = Cfg::kNodes;
   constexpr int S = Cfg::kEPB * NN;  // record-plane stride
@@ -164,7 +171,7 @@ __device__ __forceinline__ void line_work(const double* __restrict__ rec, int el
 #endif
     }
     double f[K][5];
-    chandrashekar_cart_k<K>(A, B, c_gamma, f);
+    chandrashekar_cart_v2<K>(A, B, gm1, f);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       if (k0 + k >= P) break;
@@ -190,7 +197,6 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
     euler_cartesian_kernel(int64_t E, const DMat<N> Dm, double gm1, double c_gamma,
                            double gam_ratio, const double* __restrict__ U,
                            double* __restrict__ R) {
-  const double c_hbeta = 0.5 * c_gamma;  // 1 / (4 (gamma - 1))
   using Cfg = EulerCartCfg<N>;
   constexpr int NN = Cfg::kNodes;
   constexpr int EPB = Cfg::kEPB;
@@ -236,7 +242,7 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
 #if SFB_EXP_NO_LINE
       if (active) { for (int a = 0; a < N; ++a) { o.pos[a] = a; for (int v = 0; v < 5; ++v) o.acc[a][v] = rec[a]; } }
 #else
-      if (active) line_work<N>(rec, el, dir, L, Dm, c_gamma, o);
+      if (active) line_work<N>(rec, el, dir, L, Dm, gm1, o);
 #endif
       if (active) {
         double* rs = resb + dir * kVals + el * 5 * NN;
@@ -356,7 +362,7 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
         const double X = fma(rho, et, -0.5 * mm);
         const double iX = rcp_refined(X);
         const double p = (2.0 * gm1) * X * hirho;
-        const double hbeta = (rho * rho) * (c_hbeta * iX);  // beta/2 = rho^2 / (4 (gamma-1) X)
+        const double hbeta = (rho * rho) * (0.5 * iX);  // (gamma-1) beta = rho^2 / (2X)
         const int c0 = r % N, c1 = (r / N) % N, c2 = r / (N * N);
         const int q = el * NN + swz<N>(c0, c1, c2);
         rec[q] = 0.5 * rho;
@@ -364,8 +370,8 @@ __global__ void __launch_bounds__(EulerCartCfg<N>::kThreads, EulerCartCfg<N>::kM
         rec[2 * S + q] = m1 * hirho;
         rec[3 * S + q] = m2 * hirho;
         rec[4 * S + q] = hbeta;
-        rec[5 * S + q] = log_half(rho);
-        rec[6 * S + q] = log_half(2.0 * hbeta);
+        rec[5 * S + q] = SFB_GENERIC_TABLOG ? log_half_tab(rho) : log_half(rho);
+        rec[6 * S + q] = SFB_GENERIC_TABLOG ? log_half_tab(hbeta) : log_half(hbeta);
         rec[7 * S + q] = p;
       }
       nbar_arrive(REC_FULL + s, kAll);
