@@ -33,6 +33,9 @@
 #ifndef SFB_MODAL_MINBLOCKS_N6
 #define SFB_MODAL_MINBLOCKS_N6 2
 #endif
+#ifndef SFB_MODAL_TABLOG
+#define SFB_MODAL_TABLOG 0  // table log measured 47.6 vs 47.0 ms here
+#endif
 #ifndef SFB_MODAL_COMPACT
 #define SFB_MODAL_COMPACT 0  // 1: 69 KB smem but one more barrier: 51.0 vs 47.9 ms
 #endif
@@ -295,8 +298,8 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
       rec[2 * NN + r] = m1 * hirho;
       rec[3 * NN + r] = m2 * hirho;
       rec[4 * NN + r] = hbeta;
-      rec[5 * NN + r] = log_half_tab(rho);
-      rec[6 * NN + r] = log_half_tab(hbeta);
+      rec[5 * NN + r] = SFB_MODAL_TABLOG ? log_half_tab(rho) : log_half(rho);
+      rec[6 * NN + r] = SFB_MODAL_TABLOG ? log_half_tab(hbeta) : log_half(hbeta);
       // n_diag = sum_i D[r_i,r_i] Ja^i(r); diagonal term f(u).n_diag with
       // mass = m.n_diag, w = mass / rho:  (mass, w m + p n_diag, (E + p) w)
       const int c0 = r % N, c1 = (r / N) % N, c2 = r / (N * N);
