@@ -22,6 +22,9 @@
 // (a lane's x0 line is n contiguous doubles of every variable).
 #include "euler_common.cuh"
 
+#ifndef SFB_WARP_TABLOG
+#define SFB_WARP_TABLOG 1
+#endif
 #ifndef SFB_WARP_MINBLOCKS_N4
 #define SFB_WARP_MINBLOCKS_N4 12
 #endif
@@ -175,7 +178,8 @@ __global__ void __launch_bounds__(32, WarpCfg<N>::kMinBlocks)
       const double hbeta = (rho * rho) * iX2;  // (gamma - 1) beta = rho^2 / (2X)
       const int c0 = r % N, c1 = (r / N) % N, c2 = r / L2;
       const int q = e * NN + swz<N>(c0, c1, c2);
-      const double lr = log_half_tab(rho), lb = log_half_tab(hbeta);
+      const double lr = SFB_WARP_TABLOG ? log_half_tab(rho) : log_half(rho);
+      const double lb = SFB_WARP_TABLOG ? log_half_tab(hbeta) : log_half(hbeta);
       // diagonal term sum_j D_{c_j c_j} f_j(u, u): with mass = D.m and
       // w = mass / rho:  (mass, w m + p D, (E + p) w)
       const double d0 = dd0, d1 = dd1, d2 = ddiag[c2];
