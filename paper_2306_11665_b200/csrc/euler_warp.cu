@@ -22,6 +22,12 @@
 // (a lane's x0 line is n contiguous doubles of every variable).
 #include "euler_common.cuh"
 
+#ifndef SFB_WARP_OWN
+#define SFB_WARP_OWN 1
+#endif
+#ifndef SFB_WARP_OWN_MINBLOCKS_N4
+#define SFB_WARP_OWN_MINBLOCKS_N4 11
+#endif
 #ifndef SFB_WARP_TABLOG
 #define SFB_WARP_TABLOG 1
 #endif
@@ -46,20 +52,17 @@ struct WarpCfg {
   static constexpr int kK = N == 2 ? 1 : (N == 4 ? SFB_WARP_K_N4 : (N == 3 ? 3 : 2));
   static constexpr int kMinBlocks =
       N == 2 ? 24 : (N == 3 ? 16 : (N == 4 ? SFB_WARP_MINBLOCKS_N4 : 12));
+  static constexpr size_t kSmemOwn = (size_t)17 * kS * sizeof(double);  // rec + 2 buffers
+  static constexpr int kMinBlocksOwn =
+      N == 2 ? 24 : (N == 3 ? 16 : (N == 4 ? SFB_WARP_OWN_MINBLOCKS_N4 : 10));
 };
 
-// Accumulate the pairs of one line (nodes pos[0..N-1] in the swizzled record
+// The node records of one line (nodes pos[0..N-1] in the swizzled record
 // planes, velocity planes permuted so plane vp0 is along the line).
 template <int N>
-__device__ __forceinline__ void line_pairs(const double* __restrict__ rec, const int (&pos)[N],
-                                           int vp0, int vp1, int vp2, const DMat<N> Dm, double gm1,
-                                           double (&acc)[N][5]) {
+__device__ __forceinline__ void load_line(const double* __restrict__ rec, const int (&pos)[N],
+                                          int vp0, int vp1, int vp2, NodeRec (&nrec)[N]) {
   constexpr int S = WarpCfg<N>::kS;
-#pragma unroll
-  for (int a = 0; a < N; ++a)
-#pragma unroll
-    for (int v = 0; v < 5; ++v) acc[a][v] = 0.0;
-  NodeRec nrec[N];
 #pragma unroll
   for (int a = 0; a < N; ++a) {
     const double* pr = rec + pos[a];
@@ -72,6 +75,16 @@ __device__ __forceinline__ void line_pairs(const double* __restrict__ rec, const
     nrec[a].hlb = pr[6 * S];
     nrec[a].q = 0.0;
   }
+}
+
+// Accumulate the pairs of one line: acc[a] = sum_b D[a,b] F#(a, b).
+template <int N>
+__device__ __forceinline__ void line_pairs_regs(const NodeRec (&nrec)[N], const DMat<N> Dm,
+                                                double gm1, double (&acc)[N][5]) {
+#pragma unroll
+  for (int a = 0; a < N; ++a)
+#pragma unroll
+    for (int v = 0; v < 5; ++v) acc[a][v] = 0.0;
   constexpr PairOrder<N> po;
   constexpr int P = PairOrder<N>::kPairs;
   constexpr int K = WarpCfg<N>::kK;
@@ -99,6 +112,15 @@ __device__ __forceinline__ void line_pairs(const double* __restrict__ rec, const
       }
     }
   }
+}
+
+template <int N>
+__device__ __forceinline__ void line_pairs(const double* __restrict__ rec, const int (&pos)[N],
+                                           int vp0, int vp1, int vp2, const DMat<N> Dm, double gm1,
+                                           double (&acc)[N][5]) {
+  NodeRec nrec[N];
+  load_line<N>(rec, pos, vp0, vp1, vp2, nrec);
+  line_pairs_regs<N>(nrec, Dm, gm1, acc);
 }
 
 template <int N>
@@ -250,24 +272,207 @@ __global__ void __launch_bounds__(32, WarpCfg<N>::kMinBlocks)
   }
 }
 
+// Variant "own line" (SFB_WARP_OWN): a lane's record nodes are the nodes of
+// its own x0 line, so (1) the x0 lines run first, straight from the records in
+// registers (no shared loads), (2) the diagonal term and the x0 result stay in
+// the lane's registers until the store, and (3) the x2 / x1 results are plain
+// stores into two buffers read once by the owning lane: 164 instead of 232
+// shared-memory accesses per lane and block, for 20 more live registers.
+// Sum order per node: ((diag + x0) + x2) + x1.
+template <int N>
+__global__ void __launch_bounds__(32, WarpCfg<N>::kMinBlocksOwn)
+    euler_cart_own_kernel(int64_t E, const DMat<N> Dm, double gm1, const double* __restrict__ U,
+                          double* __restrict__ R) {
+  using Cfg = WarpCfg<N>;
+  constexpr int NN = Cfg::kNN, L2 = Cfg::kL2, EPW = Cfg::kEPW, A = Cfg::kActive, S = Cfg::kS;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double ddiag[N];
+  const int lane = threadIdx.x;
+  double* rec = smem;          // [7][S]
+  double* bx2 = rec + 7 * S;   // [5][S] x2-line results
+  double* bx1 = bx2 + 5 * S;   // [5][S] x1-line results
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) ddiag[i] = Dm.d[i * (N + 1)];
+  }
+  __syncwarp();
+
+  const int64_t nwb = (E + EPW - 1) / EPW;
+  const int64_t g = blockIdx.x;
+  const int64_t G = gridDim.x;
+  const int niter = g < nwb ? (int)((nwb - 1 - g) / G) + 1 : 0;
+  auto nel_of = [&](int64_t wb) {
+    const int64_t e0 = wb * EPW;
+    return (E - e0) < EPW ? (int)(E - e0) : EPW;
+  };
+  auto prefetch = [&](int it) {
+    const int64_t wb = g + (int64_t)it * G;
+    const uintptr_t b0 = (uintptr_t)(U + wb * EPW * 5 * NN);
+    const uintptr_t b1 = b0 + (uintptr_t)nel_of(wb) * 5 * NN * 8;
+    const uintptr_t a0 = (b0 + 15) & ~(uintptr_t)15, a1 = b1 & ~(uintptr_t)15;
+    if (a1 > a0)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0))
+                   : "memory");
+  };
+
+  const bool act = lane < A;
+  const int ln = act ? lane : 0;
+  const int el = ln / L2, L = ln - el * L2, u = L % N, w = L / N;
+  const double hgm1 = 0.5 * gm1;
+  const double* rl = rec + el * NN;
+  int pos2[N], pos1[N], pos0[N];
+#pragma unroll
+  for (int a = 0; a < N; ++a) {
+    pos0[a] = swz<N>(a, u, w);
+    pos1[a] = swz<N>(u, a, w);
+    pos2[a] = swz<N>(u, w, a);
+  }
+  const double d1 = ddiag[u], d2 = ddiag[w];
+
+  if (lane == 0 && niter > 0) prefetch(0);
+  if (lane == 0 && niter > 1) prefetch(1);
+  for (int it = 0; it < niter; ++it) {
+    const int64_t wb = g + (int64_t)it * G;
+    const int nel = nel_of(wb);
+    if (lane == 0 && it + 2 < niter) prefetch(it + 2);
+    // ---- records + diagonal term of this lane's x0 line ------------------------
+    const double* ub = U + (wb * EPW + (el < nel ? el : 0)) * 5 * NN + N * L;
+    double st[5][N];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      if constexpr (N % 2 == 0) {
+#pragma unroll
+        for (int a = 0; a < N; a += 2) {
+          const double2 x = ld_stream_d2(ub + v * NN + a);
+          st[v][a] = x.x;
+          st[v][a + 1] = x.y;
+        }
+      } else {
+#pragma unroll
+        for (int a = 0; a < N; ++a) st[v][a] = __ldcs(ub + v * NN + a);
+      }
+    }
+    NodeRec nr[N];
+    double acc0[N][5];
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+      const double rho = st[0][a], m0 = st[1][a], m1 = st[2][a], m2 = st[3][a], et = st[4][a];
+      const double irho = rcp_refined(rho);
+      const double hirho = 0.5 * irho;
+      const double mm = fma(m2, m2, fma(m1, m1, m0 * m0));
+      const double X2 = fma(rho, et + et, -mm);
+      const double iX2 = rcp_refined(X2);
+      const double p = (hgm1 * X2) * irho;
+      const double hbeta = (rho * rho) * iX2;
+      nr[a].hr = 0.5 * rho;
+      nr[a].hv0 = m0 * hirho;
+      nr[a].hv1 = m1 * hirho;
+      nr[a].hv2 = m2 * hirho;
+      nr[a].hb = hbeta;
+      nr[a].hlr = SFB_WARP_TABLOG ? log_half_tab(rho) : log_half(rho);
+      nr[a].hlb = SFB_WARP_TABLOG ? log_half_tab(hbeta) : log_half(hbeta);
+      nr[a].q = 0.0;
+      if (act) {
+        double* pr = rec + el * NN + pos0[a];
+        pr[0] = nr[a].hr;
+        pr[S] = nr[a].hv0;
+        pr[2 * S] = nr[a].hv1;
+        pr[3 * S] = nr[a].hv2;
+        pr[4 * S] = nr[a].hb;
+        pr[5 * S] = nr[a].hlr;
+        pr[6 * S] = nr[a].hlb;
+      }
+      const double d0 = Dm.d[a * (N + 1)];
+      const double mass = fma(d2, m2, fma(d1, m1, d0 * m0));
+      const double wv = mass * irho;
+      acc0[a][0] = mass;
+      acc0[a][1] = fma(wv, m0, p * d0);
+      acc0[a][2] = fma(wv, m1, p * d1);
+      acc0[a][3] = fma(wv, m2, p * d2);
+      acc0[a][4] = (et + p) * wv;
+    }
+    // ---- lines along x0, from the registers -------------------------------------
+    {
+      double acc[N][5];
+      line_pairs_regs<N>(nr, Dm, gm1, acc);
+#pragma unroll
+      for (int a = 0; a < N; ++a)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) acc0[a][v] = acc0[a][v] + acc[a][v];
+    }
+    __syncwarp();  // all records in shared memory
+    // ---- lines along x2 and x1: results to their buffers (plain stores) -------
+    {
+      double acc[N][5];
+      line_pairs<N>(rl, pos2, 3 * S, 1 * S, 2 * S, Dm, gm1, acc);
+      if (act) {
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+          double* p = bx2 + el * NN + pos2[a];
+          p[0] = acc[a][0];
+          p[3 * S] = acc[a][1];
+          p[S] = acc[a][2];
+          p[2 * S] = acc[a][3];
+          p[4 * S] = acc[a][4];
+        }
+      }
+      line_pairs<N>(rl, pos1, 2 * S, 3 * S, 1 * S, Dm, gm1, acc);
+      if (act) {
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+          double* p = bx1 + el * NN + pos1[a];
+          p[0] = acc[a][0];
+          p[2 * S] = acc[a][1];
+          p[3 * S] = acc[a][2];
+          p[S] = acc[a][3];
+          p[4 * S] = acc[a][4];
+        }
+      }
+    }
+    __syncwarp();  // x2 / x1 results visible to the owning lanes
+    if (act && el < nel) {
+      double* out = R + (wb * EPW + el) * 5 * NN + N * L;
+      const double* q2 = bx2 + el * NN;
+      const double* q1 = bx1 + el * NN;
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        double o[N];
+#pragma unroll
+        for (int a = 0; a < N; ++a)
+          o[a] = (acc0[a][v] + q2[v * S + pos0[a]]) + q1[v * S + pos0[a]];
+        if constexpr (N % 2 == 0) {
+#pragma unroll
+          for (int a = 0; a < N; a += 2) st_stream_d2(out + v * NN + a, make_double2(o[a], o[a + 1]));
+        } else {
+#pragma unroll
+          for (int a = 0; a < N; ++a) __stcs(out + v * NN + a, o[a]);
+        }
+      }
+    }
+    __syncwarp();  // buffers and records are rewritten by the next block
+  }
+}
+
 template <int N>
 int launch_euler_cart_warp(int64_t E, const double* Dh, double gamma, double scale,
                            const double* U, double* R, cudaStream_t s) {
   using Cfg = WarpCfg<N>;
   DMat<N> Dm;
   for (int i = 0; i < N * N; ++i) Dm.d[i] = scale * Dh[i];
+  constexpr bool own = SFB_WARP_OWN != 0;
+  constexpr size_t smem = own ? Cfg::kSmemOwn : Cfg::kSmem;
+  auto kern = own ? euler_cart_own_kernel<N> : euler_cart_warp_kernel<N>;
   static int per_sm = 0;
   if (per_sm == 0) {
-    cudaFuncSetAttribute(euler_cart_warp_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)Cfg::kSmem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, euler_cart_warp_kernel<N>, 32, Cfg::kSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 32, smem);
     per_sm = b > 0 ? b : 1;
   }
   const int64_t nwb = (E + Cfg::kEPW - 1) / Cfg::kEPW;
   int64_t grid = (int64_t)num_sms() * per_sm;
   if (grid > nwb) grid = nwb;
-  euler_cart_warp_kernel<N><<<(unsigned)grid, 32, Cfg::kSmem, s>>>(E, Dm, gamma - 1.0, U, R);
+  kern<<<(unsigned)grid, 32, smem, s>>>(E, Dm, gamma - 1.0, U, R);
   return check_launch("euler_volume_cartesian(warp-autonomous)");
 }
 
