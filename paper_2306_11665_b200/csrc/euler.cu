@@ -61,9 +61,6 @@
 #ifndef SFB_FUSED_N4
 #define SFB_FUSED_N4 1
 #endif
-#ifndef SFB_SPLIT_N4
-#define SFB_SPLIT_N4 0
-#endif
 #ifndef SFB_RECS_IN_REGS
 #define SFB_RECS_IN_REGS 1
 #endif
@@ -407,8 +404,6 @@ static int launch_euler_cartesian(int64_t E, const double* Dh, double gamma, dou
   return check_launch("euler_volume_cartesian");
 }
 
-int launch_euler_cart4_split(int64_t E, const double* Dh, double gamma, double scale,
-                             const double* U, double* R, cudaStream_t s);
 int launch_euler_cart4_fused(int64_t E, const double* Dh, double gamma, double scale,
                              const double* U, double* R, cudaStream_t s);
 
@@ -428,8 +423,7 @@ int euler_cartesian_dispatch(int64_t E, int64_t n, const double* D_host, double 
     case 4:
       if (SFB_WARP_N4) return launch_euler_cart_warp<4>(E, D_host, gamma, scale, U, R, s);
       if (SFB_FUSED_N4) return launch_euler_cart4_fused(E, D_host, gamma, scale, U, R, s);
-      return SFB_SPLIT_N4 ? launch_euler_cart4_split(E, D_host, gamma, scale, U, R, s)
-                          : launch_euler_cartesian<4>(E, D_host, gamma, scale, U, R, s);
+      return launch_euler_cartesian<4>(E, D_host, gamma, scale, U, R, s);
     case 5:  // warp kernel (25 of 32 lanes) measured 1.02 vs 0.85 ms: CTA kernel
       return SFB_WARP_SMALL > 1 ? launch_euler_cart_warp<5>(E, D_host, gamma, scale, U, R, s)
                                 : launch_euler_cartesian<5>(E, D_host, gamma, scale, U, R, s);

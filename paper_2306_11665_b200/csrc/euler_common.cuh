@@ -1,4 +1,4 @@
-// Pieces shared by the Cartesian Euler kernels (euler.cu, euler_split.cu).
+// Pieces shared by the Cartesian Euler kernels (euler.cu, euler_fused.cu, euler_warp.cu).
 #pragma once
 
 #include "bulk.cuh"

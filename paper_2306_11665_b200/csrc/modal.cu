@@ -462,16 +462,9 @@ static int launch_modal(int64_t E, const double* V, const double* Pi, const doub
   return check_launch("euler_volume_curvilinear_modal");
 }
 
-template <int N>
-int launch_modal_ws(int64_t E, const double* V, const double* Pi, const double* D, double gamma,
-                    double scale, const double* Uhat, const double* Ja, double* Rhat,
-                    double* sumsq, cudaStream_t s);
 
 }  // namespace sfb
 
-#ifndef SFB_MODAL_WS
-#define SFB_MODAL_WS 0
-#endif
 
 using namespace sfb;
 
@@ -493,12 +486,10 @@ extern "C" int sfb_euler_volume_curvilinear_modal(int64_t E, int64_t n, const do
     case 2: return launch_modal<2>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s);
     case 3: return launch_modal<3>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s);
     case 4:
-      return SFB_MODAL_WS ? launch_modal_ws<4>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s)
-                          : launch_modal<4>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s);
+      return launch_modal<4>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s);
     case 5: return launch_modal<5>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s);
     case 6:
-      return SFB_MODAL_WS ? launch_modal_ws<6>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s)
-                          : launch_modal<6>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s);
+      return launch_modal<6>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s);
     case 7: return launch_modal<7>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s);
     case 8: return launch_modal<8>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s);
     default: return fail(SFB_ENOTSUP, "euler_volume_curvilinear_modal: n must be in 2..8");
