@@ -273,9 +273,16 @@ def run_ours(args):
     from paper_2306_11665_b200 import euler as eu
 
     world, rank, local = dist_env()
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # SFB_DIST_BACKEND=gloo only for functional checks of the multi-rank
+        # path on a one-GPU box (never for reported numbers)
+        backend = os.environ.get("SFB_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     sampler = ClockSampler(local)
@@ -304,8 +311,8 @@ def run_ours(args):
                            flops_launch=euler_flops_per_element(n) * E,
                            extra={"element_dof_per_s": None, "dof_per_element": n**3})
         line["element_dof_per_s"] = world * E * n**3 / (line["ms_per_step"] / 1e3)
-        if rank == 0 and world == 1 and not args.no_e2e:
-            line["e2e"] = measure_e2e(args, U)
+        if not args.no_e2e:  # every rank its own host buffers; max over ranks
+            line["e2e"] = measure_e2e(args, U, world, dist, dev)
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = measure_cpu_baseline(args, U)
         if world == 1 and not args.no_extras:
@@ -502,8 +509,11 @@ def measure_other_configs(args, dev, stream, sampler, dist):
     return out
 
 
-def measure_e2e(args, U_dev):
-    """Through the C-ABI host-buffer entry: pinned host U in, pinned host R out."""
+def measure_e2e(args, U_dev, world=1, dist=None, dev=None):
+    """Through the C-ABI host-buffer entry: pinned host U in, pinned host R out.
+
+    Every rank runs its own shard; the step time is the max over ranks and the
+    value the whole job's entries per second."""
     import torch
 
     from paper_2306_11665_b200 import euler as eu
@@ -515,18 +525,25 @@ def measure_e2e(args, U_dev):
     steps = max(3, min(args.steps, 10))
     for _ in range(2):
         eu.volume_cartesian_host(Uh, n, out=Rh)
+    if world > 1:
+        dist.barrier()
     times = []
     for _ in range(steps):
         t = time.perf_counter()
         eu.volume_cartesian_host(Uh, n, out=Rh)
         times.append(time.perf_counter() - t)
     sec = float(np.mean(times))
+    if world > 1:
+        t = torch.tensor([sec], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sec = float(t.item())
     # the result is read on the host: cross-check one element against the device path
     Rd = eu.volume_cartesian(U_dev[:1].contiguous(), n).cpu()
     assert torch.equal(Rd[0], Rh[0]), "e2e result differs from the device path"
     nbytes = Uh.numel() * 8
-    return {"value": E * 3 * n**4 / sec, "unit": "entries/s", "h2d_bytes_per_step": nbytes,
-            "d2h_bytes_per_step": nbytes, "ms_per_step": sec * 1e3, "steps": steps,
+    return {"value": world * E * 3 * n**4 / sec, "unit": "entries/s",
+            "h2d_bytes_per_step": world * nbytes, "d2h_bytes_per_step": world * nbytes,
+            "ms_per_step": sec * 1e3, "steps": steps, "n_ranks": world,
             "path": "sfb_euler_volume_cartesian_host (pinned host buffers, 3-stream "
                     "chunked H2D/kernel/D2H pipeline), wall clock per call"}
 
