@@ -506,7 +506,31 @@ def measure_other_configs(args, dev, stream, sampler, dist):
             summary["residual_norm"] = ln["residual_norm"]
         out[f"config{cfg}"] = summary
         torch.cuda.empty_cache()
+    out["f3_burgers_rk4"] = measure_burgers_rk4(dev)
     return out
+
+
+def measure_burgers_rk4(dev, E=1 << 20, d=2, n=5, steps=20):
+    """RK4 on the periodic Burgers element, whole run in one launch."""
+    import torch
+
+    from paper_2306_11665_b200 import burgers as bg
+    from paper_2306_11665_b200 import euler as eu
+
+    u0 = eu.generate_uniform(E * n**d, 11, -1.0, 1.0, device=dev).reshape(E, n**d)
+    bg.integrate_rk4(u0[:1024], d, n, 1e-3, 2, every=1)  # warm-up / operator cache
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    u, ent, mass = bg.integrate_rk4(u0, d, n, 1e-3, steps, every=steps)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    drift = float(((ent[:, -1] - ent[:, 0]).abs() / ent[:, 0]).max())
+    return {"workload": f"periodic Burgers d={d} n={n}, {E} elements, {steps} RK4 steps "
+                        f"(4 time derivatives each), entropy monitored on device",
+            "value": E * steps / (ms / 1e3), "unit": "element-steps/s", "ms": ms,
+            "launches": 1, "max_rel_entropy_drift_ec": drift}
 
 
 def measure_e2e(args, U_dev, world=1, dist=None, dev=None):
