@@ -179,3 +179,32 @@ def test_log_mean_branch_band_matches_oracle():
     # per element against the flux scale (the residual itself shrinks with amp)
     scale = np.abs(U.cpu().numpy()).max(axis=(1, 2)) ** 2
     assert (np.abs(R - ref).max(axis=(1, 2)) <= 1e-13 * scale).all()
+
+
+@pytest.mark.parametrize("n", [2, 4, 6])
+def test_non_physical_state_is_contained(n):
+    # a negative density (non-physical) makes that element's logarithms NaN;
+    # the kernels are branch-free, so the NaN stays in that element and the
+    # others are untouched (no trap, no cross-element contamination)
+    E = 37
+    U = eu.generate_states(E, n, seed=8)
+    ref = eu.volume_cartesian(U, n).cpu()
+    bad = 17
+    U[bad, 0, 3] = -U[bad, 0, 3]
+    R = eu.volume_cartesian(U, n).cpu()
+    assert torch.isnan(R[bad]).any()
+    keep = [e for e in range(E) if e != bad]
+    assert torch.equal(R[keep], ref[keep])
+
+
+def test_misaligned_pointer_rejected():
+    from paper_2306_11665_b200 import _lib
+
+    n, E = 4, 8
+    U = eu.generate_states(E + 1, n, seed=2).reshape(-1)
+    R = torch.empty_like(U)
+    _, D, _, _ = eu.gll_operators(n)
+    Dh = np.ascontiguousarray(D)
+    with pytest.raises(ValueError):  # 8-byte offset: not 16-byte aligned
+        _lib.call("sfb_euler_volume_cartesian", E, n, Dh.ctypes.data, 1.4, 2.0,
+                  _lib.ptr(U) + 8, _lib.ptr(R), _lib.stream_ptr())
