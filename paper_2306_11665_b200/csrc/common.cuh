@@ -88,7 +88,6 @@ __device__ __forceinline__ void st_stream_d2(double* p, double2 v) {
                : "memory");
 }
 
-__host__ __device__ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
 
 }  // namespace sfb
 

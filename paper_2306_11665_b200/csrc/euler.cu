@@ -131,8 +131,7 @@ __device__ __forceinline__ void line_work(const double* __restrict__ rec, int el
     q.hv2 = p[o.vplane[2]];
     q.hb = p[4 * S];
     q.hlr = p[5 * S];
-    q.hlb = p[6 * S];
-    q.q = 0.0;  // unused: the energy flux uses 2 (v_a/2).(v_b/2)
+    q.hlb = p[6 * S];  // unused: the energy flux uses 2 (v_a/2).(v_b/2)
     return q;
   };
 #pragma unroll

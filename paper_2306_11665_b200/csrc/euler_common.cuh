@@ -21,10 +21,6 @@ __device__ __forceinline__ int swz(int r0, int r1, int r2) {
   return r2 * N * N + a + N * b;
 }
 
-template <int N>
-__device__ __forceinline__ int swz_flat(int r) {
-  return swz<N>(r % N, (r / N) % N, r / (N * N));
-}
 
 // Cartesian Chandrashekar flux for K independent pairs at once, in the
 // direction-rotated frame: the callers load the velocity components permuted

@@ -25,61 +25,18 @@
 namespace sfb {
 
 
-// Coefficients of 2 atanh(f)/f - 2 = sum_k 2/(2k+3) f^(2k+2) (k = 0..8) plus
-// ln 2 split hi/lo.  In __constant__ memory so the DFMAs take them as
-// constant-bank operands instead of re-materialising 64-bit immediates.
-__constant__ double kLogPoly[11] = {
-    2.0 / 3.0,  2.0 / 5.0,  2.0 / 7.0,  2.0 / 9.0,  2.0 / 11.0, 2.0 / 13.0,
-    2.0 / 15.0, 2.0 / 17.0, 2.0 / 19.0, 6.93147180369123816490e-01, 1.90821492927058770002e-10};
-
-// Natural log for the per-node logarithms: x = 2^e m, m in [sqrt(1/2), sqrt(2)),
-// ln m = 2 atanh(f), f = (m-1)/(m+1), |f| <= 0.1716, degree-19 odd series
-// (truncation < 2.5e-17 relative).  ~22 FP64 operations, within ~2 ulp of the
-// correctly rounded value.  Branch-free (a branch would split the caller's
-// basic block and stop ptxas from interleaving independent nodes): inputs that
-// are not positive normal finite numbers - non-physical states - return NaN.
-__device__ __forceinline__ double log_pos(double x) {
-  const bool ok = x >= 2.2250738585072014e-308 && x <= 1.7976931348623157e308;
-  const int hi = __double2hiint(x), lo = __double2loint(x);
-  int e = (hi >> 20) - 1023;
-  int mh = (hi & 0x000fffff) | 0x3ff00000;
-  const bool big = mh > 0x3ff6a09e;  // m > sqrt(2)
-  mh = big ? mh - 0x00100000 : mh;
-  e = big ? e + 1 : e;
-  const double m = __hiloint2double(mh, lo);
-  const double num = m - 1.0;  // exact (Sterbenz)
-  const double den = m + 1.0;
-  const double r = rcp_refined(den);
-  double f = num * r;
-  f = fma(r, fma(-f, den, num), f);
-  const double f2 = f * f;
-  // Estrin evaluation of the degree-8 polynomial in f2 (depth 4 instead of 8)
-  const double f4 = f2 * f2;
-  const double f8 = f4 * f4;
-  const double q01 = fma(kLogPoly[1], f2, kLogPoly[0]);
-  const double q23 = fma(kLogPoly[3], f2, kLogPoly[2]);
-  const double q45 = fma(kLogPoly[5], f2, kLogPoly[4]);
-  const double q67 = fma(kLogPoly[7], f2, kLogPoly[6]);
-  const double q03 = fma(q23, f4, q01);
-  const double q47 = fma(q67, f4, q45);
-  const double p = fma(fma(kLogPoly[8], f8, q47), f8, q03);
-  const double lnm = fma(f * f2, p, f + f);
-  const double de = (double)e;
-  const double res = fma(de, kLogPoly[9], fma(de, kLogPoly[10], lnm));
-  return dsel(ok, res, __longlong_as_double(0x7ff8000000000000ll));
-}
-
 // Per-node record, all entries pre-scaled so that pair sums are exact means.
 struct NodeRec {
-  double hr;       // rho / 2
+  double hr;             // rho / 2
   double hv0, hv1, hv2;  // v / 2
-  double hb;       // beta / 2
-  double hlr;      // ln(rho) / 2
-  double hlb;      // ln(beta) / 2
-  double q;        // |v|^2 / 4 (legacy; the flux uses 2 (v_a/2).(v_b/2))
+  double hb;             // (gamma-1) beta for chandrashekar_cart_v2 / the modal flux;
+                         // beta / 2 for chandrashekar_cart_k (euler_fused.cu)
+  double hlr;            // ln(rho) / 2
+  double hlb;            // ln(hb) / 2 (v2) or ln(beta) / 2 (cart_k): only differences are used
 };
 
-// Coefficients of the log series above, halved (log_half returns ln(x)/2).
+// Coefficients of ln(m)/2 = atanh(f) = f + f^3 (1/3 + f^2/5 + ...), f = (m-1)/(m+1),
+// plus ln2/2 split hi/lo (log_half returns ln(x)/2).
 __constant__ double kLogPolyHalf[11] = {
     1.0 / 3.0,  1.0 / 5.0,  1.0 / 7.0,  1.0 / 9.0,  1.0 / 11.0, 1.0 / 13.0,
     1.0 / 15.0, 1.0 / 17.0, 1.0 / 19.0, 3.46573590184561908245e-01, 9.54107464635293850010e-11};
@@ -223,40 +180,6 @@ __device__ __forceinline__ void chandrashekar_cart_v2(const NodeRec* const (&A)[
     const double dot = fma(A[k]->hv2, B[k]->hv2, fma(A[k]->hv1, B[k]->hv1, A[k]->hv0 * B[k]->hv0));
     f[k][4] = fma(f1, fma(2.0, dot, cibeta), phat * vn);
   }
-}
-
-// Two-point flux between node records a and b for the (unnormalised)
-// direction vector (n0, n1, n2).  Output f[5].
-__device__ __forceinline__ void chandrashekar(const NodeRec& a, const NodeRec& b, double n0,
-                                              double n1, double n2, double c_gamma,
-                                              double f[5]) {
-  double vb0 = a.hv0 + b.hv0;
-  double vb1 = a.hv1 + b.hv1;
-  double vb2 = a.hv2 + b.hv2;
-  double nr, dr, nb, db;
-  logmean_parts(a.hr, b.hr, a.hlr, b.hlr, nr, dr);  // rho_ln = nr/dr
-  logmean_parts(a.hb, b.hb, a.hlb, b.hlb, nb, db);  // beta_ln = nb/db
-  double sr = a.hr + b.hr;                          // rhobar
-  double sb = a.hb + b.hb;                          // betabar
-  // one reciprocal for 1/dr, 1/nb, 1/sb
-  double p1 = dr * nb;
-  double rr = rcp_refined(p1 * sb);
-  double inv_sb = rr * p1;
-  double t = rr * sb;
-  double inv_dr = t * nb;
-  double inv_nb = t * dr;
-  double rho_ln = nr * inv_dr;
-  double ibeta = db * inv_nb;       // 1 / beta_ln
-  double phat = 0.5 * sr * inv_sb;  // rhobar / (2 betabar)
-  double vn = fma(vb2, n2, fma(vb1, n1, vb0 * n0));
-  double f1 = rho_ln * vn;
-  f[0] = f1;
-  f[1] = fma(f1, vb0, phat * n0);
-  f[2] = fma(f1, vb1, phat * n1);
-  f[3] = fma(f1, vb2, phat * n2);
-  double vv = fma(vb2, vb2, fma(vb1, vb1, vb0 * vb0));
-  double g = fma(c_gamma, ibeta, vv - (a.q + b.q));
-  f[4] = fma(f1, g, phat * vn);
 }
 
 }  // namespace sfb

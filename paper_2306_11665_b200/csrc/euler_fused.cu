@@ -140,7 +140,6 @@ __global__ void __launch_bounds__(Fused4Cfg::kThreads, SFB_FUSED_MINBLOCKS)
         nrec[a].hb = pr[4 * S];
         nrec[a].hlr = pr[5 * S];
         nrec[a].hlb = pr[6 * S];
-        nrec[a].q = 0.0;
       }
       constexpr PairOrder<N> po;
       constexpr int P = PairOrder<N>::kPairs;

@@ -73,7 +73,6 @@ __device__ __forceinline__ void load_line(const double* __restrict__ rec, const 
     nrec[a].hb = pr[4 * S];
     nrec[a].hlr = pr[5 * S];
     nrec[a].hlb = pr[6 * S];
-    nrec[a].q = 0.0;
   }
 }
 
@@ -371,7 +370,6 @@ __global__ void __launch_bounds__(32, WarpCfg<N>::kMinBlocksOwn)
       nr[a].hb = hbeta;
       nr[a].hlr = SFB_WARP_TABLOG ? log_half_tab(rho) : log_half(rho);
       nr[a].hlb = SFB_WARP_TABLOG ? log_half_tab(hbeta) : log_half(hbeta);
-      nr[a].q = 0.0;
       if (act) {
         double* pr = rec + el * NN + pos0[a];
         pr[0] = nr[a].hr;

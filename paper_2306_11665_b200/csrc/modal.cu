@@ -349,7 +349,6 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
           q.hb = rec[4 * NN + k];
           q.hlr = rec[5 * NN + k];
           q.hlb = rec[6 * NN + k];
-          q.q = 0.0;
           return q;
         };
 #pragma unroll
