@@ -49,6 +49,31 @@
 #ifndef SFB_WARP_N4
 #define SFB_WARP_N4 1  // warp-autonomous kernel (euler_warp.cu)
 #endif
+// per-n tuning of the CTA kernel (config-4 sweep; defaults measured best)
+#ifndef SFB_EPB_N6
+#define SFB_EPB_N6 2
+#endif
+#ifndef SFB_MB_N5
+#define SFB_MB_N5 2
+#endif
+#ifndef SFB_MB_N6
+#define SFB_MB_N6 1
+#endif
+#ifndef SFB_MB_N8
+#define SFB_MB_N8 1
+#endif
+#ifndef SFB_K_N5
+#define SFB_K_N5 1
+#endif
+#ifndef SFB_K_N6
+#define SFB_K_N6 2
+#endif
+#ifndef SFB_K_N7
+#define SFB_K_N7 1
+#endif
+#ifndef SFB_K_N8
+#define SFB_K_N8 2
+#endif
 #ifndef SFB_GENERIC_TABLOG
 #define SFB_GENERIC_TABLOG 0  // table log: +30% at n=6 (the single prep warp is latency-bound)
 #endif
@@ -77,14 +102,16 @@ struct EulerCartCfg {
   // elements per block; line threads = 3 EPB N^2 (padded to warps), chosen so
   // the padding is small and the line warps are direction-uniform for N = 4
   // (EPB*5*N^3*8 bytes must be a multiple of 16 for the 1-D bulk copy)
-  static constexpr int kEPB = (N == 2) ? 8 : (N == 3) ? 8 : (N >= 7) ? 1 : 2;
+  static constexpr int kEPB = (N == 2) ? 8 : (N == 3) ? 8 : (N >= 7) ? 1 : (N == 6 ? SFB_EPB_N6 : 2);
   static constexpr int kLineThreads = 3 * kLines * kEPB;
   static constexpr int kLineWarps = (kLineThreads + 31) / 32;
   // prep warps balance node preprocessing + stores against the line work
   static constexpr int kPrepWarps = (N <= 3) ? 3 : (N == 4 ? SFB_PREP_WARPS_N4 : 1);
   static constexpr int kThreads = 32 * (kLineWarps + kPrepWarps);
   static constexpr int kMinBlocks =
-      (N == 4) ? SFB_MINBLOCKS_N4 : (N == 7 ? SFB_MINBLOCKS_N7 : ((N == 5 || N == 3) ? 2 : 1));
+      (N == 4) ? SFB_MINBLOCKS_N4
+               : (N == 7 ? SFB_MINBLOCKS_N7
+                         : (N == 6 ? SFB_MB_N6 : (N == 8 ? SFB_MB_N8 : (N == 5 ? SFB_MB_N5 : 2))));
   static constexpr int kVals = kEPB * 5 * kNodes;  // doubles per block of states
   static constexpr int kPlanes = 8;                // 7 record planes + pressure
   static constexpr int kRecVals = kPlanes * kEPB * kNodes;
@@ -96,7 +123,12 @@ struct EulerCartCfg {
 
 // pairs evaluated side by side per line thread (ILP knob)
 template <int N>
-constexpr int kPairBatch = (N == 4) ? SFB_PAIR_BATCH_N4 : ((N == 5 || N == 7) ? 1 : 2);
+constexpr int kPairBatch = (N == 4)   ? SFB_PAIR_BATCH_N4
+                           : (N == 5) ? SFB_K_N5
+                           : (N == 6) ? SFB_K_N6
+                           : (N == 7) ? SFB_K_N7
+                           : (N == 8) ? SFB_K_N8
+                                      : 2;
 
 template <int N>
 struct LineOut {
