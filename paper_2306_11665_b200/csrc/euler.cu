@@ -81,7 +81,7 @@
 #define SFB_MINBLOCKS_N7 1  // 2 caps at 168 regs and spills (1.86 vs 1.54 ms at config 4)
 #endif
 #ifndef SFB_WARP_SMALL
-#define SFB_WARP_SMALL 1  // 1: n = 2 on the warp-autonomous kernel; 2: n = 3, 5 too
+#define SFB_WARP_SMALL 1  // 1: n = 2, 3 on the warp-autonomous kernel; 2: n = 5 too
 #endif
 #ifndef SFB_FUSED_N4
 #define SFB_FUSED_N4 1
@@ -448,14 +448,14 @@ int euler_cartesian_dispatch(int64_t E, int64_t n, const double* D_host, double 
     case 2:
       return SFB_WARP_SMALL ? launch_euler_cart_warp<2>(E, D_host, gamma, scale, U, R, s)
                             : launch_euler_cartesian<2>(E, D_host, gamma, scale, U, R, s);
-    case 3:  // warp kernel measured 0.673 vs 0.657 ms (config 4): CTA kernel
-      return SFB_WARP_SMALL > 1 ? launch_euler_cart_warp<3>(E, D_host, gamma, scale, U, R, s)
-                                : launch_euler_cartesian<3>(E, D_host, gamma, scale, U, R, s);
+    case 3:  // own-line warp kernel 0.552 vs CTA kernel 0.663 ms (config 4)
+      return SFB_WARP_SMALL ? launch_euler_cart_warp<3>(E, D_host, gamma, scale, U, R, s)
+                            : launch_euler_cartesian<3>(E, D_host, gamma, scale, U, R, s);
     case 4:
       if (SFB_WARP_N4) return launch_euler_cart_warp<4>(E, D_host, gamma, scale, U, R, s);
       if (SFB_FUSED_N4) return launch_euler_cart4_fused(E, D_host, gamma, scale, U, R, s);
       return launch_euler_cartesian<4>(E, D_host, gamma, scale, U, R, s);
-    case 5:  // warp kernel (25 of 32 lanes) measured 1.02 vs 0.85 ms: CTA kernel
+    case 5:  // warp kernel (25 of 32 lanes) measured 0.98 vs 0.84 ms: CTA kernel
       return SFB_WARP_SMALL > 1 ? launch_euler_cart_warp<5>(E, D_host, gamma, scale, U, R, s)
                                 : launch_euler_cartesian<5>(E, D_host, gamma, scale, U, R, s);
     case 6: return launch_euler_cartesian<6>(E, D_host, gamma, scale, U, R, s);

@@ -28,6 +28,9 @@
 #ifndef SFB_WARP_OWN_MINBLOCKS_N4
 #define SFB_WARP_OWN_MINBLOCKS_N4 11
 #endif
+#ifndef SFB_WARP_OWN_MINBLOCKS_N5
+#define SFB_WARP_OWN_MINBLOCKS_N5 8
+#endif
 #ifndef SFB_WARP_TABLOG
 #define SFB_WARP_TABLOG 1
 #endif
@@ -54,7 +57,7 @@ struct WarpCfg {
       N == 2 ? 24 : (N == 3 ? 16 : (N == 4 ? SFB_WARP_MINBLOCKS_N4 : 12));
   static constexpr size_t kSmemOwn = (size_t)17 * kS * sizeof(double);  // rec + 2 buffers
   static constexpr int kMinBlocksOwn =
-      N == 2 ? 24 : (N == 3 ? 16 : (N == 4 ? SFB_WARP_OWN_MINBLOCKS_N4 : 10));
+      N == 2 ? 24 : (N == 3 ? 16 : (N == 4 ? SFB_WARP_OWN_MINBLOCKS_N4 : SFB_WARP_OWN_MINBLOCKS_N5));
 };
 
 // The node records of one line (nodes pos[0..N-1] in the swizzled record
