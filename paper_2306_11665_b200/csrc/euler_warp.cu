@@ -1,4 +1,4 @@
-// K3, warp-autonomous (n = 2..5): every warp owns a private pipeline over a
+// K3, warp-autonomous (n = 2..5; the default for n = 2, 3, 4): every warp owns a private pipeline over a
 // block of EPW = floor(32 / n^2) elements and never waits on another warp.
 //
 // Why: the CTA-wide variants (euler.cu, euler_fused.cu) map one thread to one
