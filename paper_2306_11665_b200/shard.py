@@ -15,7 +15,6 @@ divides the block count.  ``allreduce=True`` instead sums one scalar per rank
 with all_reduce (the plain NCCL reduction; not G-invariant in the last bits).
 """
 
-import numpy as np
 import torch
 
 from . import _lib
