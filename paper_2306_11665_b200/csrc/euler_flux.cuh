@@ -112,17 +112,18 @@ __device__ __forceinline__ double log_half_tab(double x) {
 
 // Numerator / denominator of the log mean of (x, y) = (2 hx, 2 hy) (or any
 // exact rescaling): L = num / den.
-//   series branch:  num = s s^2,  den = s^2 + d^2 (1/3 + u/5),  u = d^2/s^2
-//   log branch:     num = d,      den = (ln y - ln x)/2        (per-node logs)
-// i.e. s / (1 + u/3 + u^2/5) scaled by s^2, so u is only needed inside the
-// correction, where the raw MUFU reciprocal (rel. err ~2^-22) costs < 1e-16.
+//   series branch:  num = s (s^2 - 3/5 d^2),  den = s^2 - 4/15 d^2
+//   log branch:     num = d,                  den = (ln y - ln x)/2  (per-node logs)
+// The series branch is the [1/1] Pade approximant in u = d^2/s^2 of
+// L/s = 1 / (1 + u/3 + u^2/5 + u^3/7 + ...): (1 - 3u/5) / (1 - 4u/15), exact
+// through u^2 with an O(u^3) remainder below 2e-16 relative for u <= 2e-5
+// (checked against 50-digit logarithms) - no reciprocal, no MUFU in the chain.
 // Branch test: integer comparison of the IEEE high words of d^2 and s^2,
 // series iff hi(d^2) - hi(s^2) < -(hi(1.0) - hi(1e-5)), i.e. u below ~1e-5 -
 // the test of the oracle (oracle/euler_oracle.py:series_branch, euler_oracle.c)
-// verbatim, on the ALU (no FP64 compare).  Under it the truncated u^3/7 term is
-// < 2e-16 relative; above it the per-node log difference loses at most
-// ~|ln x| 1e-16 / (2|d/s|), |d/s| >= 3e-3 -> < 4e-14 relative.  The final
-// division happens in the caller's combined reciprocal.
+// verbatim, on the ALU (no FP64 compare).  Above it the per-node log
+// difference loses at most ~|ln x| 1e-16 / (2|d/s|), |d/s| >= 3e-3 -> < 4e-14
+// relative.  The final division happens in the caller's combined reciprocal.
 __device__ __forceinline__ void logmean_parts(double hx, double hy, double hlx, double hly,
                                               double& num, double& den) {
   const double d = __dsub_rn(hy, hx);
@@ -130,9 +131,8 @@ __device__ __forceinline__ void logmean_parts(double hx, double hy, double hlx, 
   const double d2 = __dmul_rn(d, d);
   const double s2 = __dmul_rn(s, s);
   const bool series = (__double2hiint(d2) - __double2hiint(s2)) < -(int)(0x3ff00000 - 0x3ee4f8b5);
-  const double q = fma(d2 * rcp_approx(s2), 0.2, 1.0 / 3.0);
-  num = dsel(series, s * s2, d);
-  den = dsel(series, fma(d2, q, s2), __dsub_rn(hly, hlx));
+  num = dsel(series, s * fma(d2, -0.6, s2), d);
+  den = dsel(series, fma(d2, -4.0 / 15.0, s2), __dsub_rn(hly, hlx));
 }
 
 // Cartesian flux for K pairs on records whose beta entries are pre-scaled by
