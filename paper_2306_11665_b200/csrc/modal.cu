@@ -33,6 +33,9 @@
 #ifndef SFB_MODAL_MINBLOCKS_N6
 #define SFB_MODAL_MINBLOCKS_N6 2
 #endif
+#ifndef SFB_MODAL_PARITY
+#define SFB_MODAL_PARITY 1  // even/odd transforms when the operators have the parity
+#endif
 #ifndef SFB_MODAL_TABLOG
 #define SFB_MODAL_TABLOG 0  // table log measured 47.6 vs 47.0 ms here
 #endif
@@ -71,51 +74,81 @@ struct ModalCfg {
   static constexpr int kMinBlocks = (N == 6) ? SFB_MODAL_MINBLOCKS_N6 : 1;
 };
 
-// One sum-factorised pass along direction j:
-//   out[.., a_j, ..] = sum_c A[a_j][c] in[.., c, ..]
-// A is a reference into the __grid_constant__ parameter block, so with the
-// loops unrolled every coefficient is a constant-bank operand of its DFMA (no
-// shared-memory load per multiply: 56 -> 52.5 ms at config 5).  One work item
-// per (variable, line); splitting a line's outputs over two items to fill the
-// CTA more evenly measured slower (58.8 ms: the inputs are loaded twice).
-template <int N>
-__device__ __forceinline__ void kron_pass(const double (&A)[N * N], int j,
-                                          const double* __restrict__ in, double* __restrict__ out,
-                                          int tid, int nthreads) {
-  constexpr int NN = N * N * N;
-  const int stride = j == 0 ? 1 : (j == 1 ? N : N * N);
-  for (int t = tid; t < 5 * N * N; t += nthreads) {
-    const int v = t / (N * N);
-    const int L = t - v * N * N;
-    const int u0 = L % N, u1 = L / N;
-    int base;
-    if (j == 0) base = u0 * N + u1 * N * N;
-    else if (j == 1) base = u0 + u1 * N * N;
-    else base = u0 + u1 * N;
-    const double* src = in + v * NN + base;
-    double x[N];
+// y = A x along one line, dense or exploiting the parity of the Legendre /
+// GLL operators (x_{n-1-i} = -x_i, P_k(-x) = (-1)^k P_k(x)):
+//   MODE 1, V (modal -> nodal): V[n-1-i][k] = (-1)^k V[i][k], so with the even
+//     and odd modal sums e_i, o_i over the first n/2 nodes y_i = e_i + o_i and
+//     y_{n-1-i} = e_i - o_i (n/2 rows of n FMAs instead of n rows);
+//   MODE 2, Pi = V^-1 (nodal -> modal): Pi[k][n-1-i] = (-1)^k Pi[k][i], so the
+//     nodal sums s_i = x_i + x_{n-1-i} feed the even modes and the differences
+//     t_i = x_i - x_{n-1-i} the odd ones (n rows of n/2 FMAs).
+// At n = 6: 18 FMAs + 6 adds per line instead of 36 FMAs.  The host takes the
+// symmetric path only when the given operators have the parity to 1e-13
+// (they do when built by the reference's constructors, operators.py:96-232).
+template <int N, int MODE>
+__device__ __forceinline__ void apply_line(const double (&A)[N * N], const double (&x)[N],
+                                           double (&y)[N]) {
+  constexpr int H = N / 2;
+  if constexpr (MODE == 1) {
 #pragma unroll
-    for (int c = 0; c < N; ++c) x[c] = src[c * stride];
-    double* dst = out + v * NN + base;
+    for (int i = 0; i < H; ++i) {
+      double e = 0.0, o = 0.0;
+#pragma unroll
+      for (int k = 0; k < N; k += 2) e = fma(A[i * N + k], x[k], e);
+#pragma unroll
+      for (int k = 1; k < N; k += 2) o = fma(A[i * N + k], x[k], o);
+      y[i] = e + o;
+      y[N - 1 - i] = e - o;
+    }
+    if constexpr (N % 2 == 1) {
+      double e = 0.0;
+#pragma unroll
+      for (int k = 0; k < N; k += 2) e = fma(A[H * N + k], x[k], e);
+      y[H] = e;
+    }
+  } else if constexpr (MODE == 2) {
+    double sm[H > 0 ? H : 1], df[H > 0 ? H : 1];
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      sm[i] = x[i] + x[N - 1 - i];
+      df[i] = x[i] - x[N - 1 - i];
+    }
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      double acc = 0.0;
+#pragma unroll
+      for (int i = 0; i < H; ++i) acc = fma(A[k * N + i], (k % 2 == 0) ? sm[i] : df[i], acc);
+      if constexpr (N % 2 == 1) {
+        if (k % 2 == 0) acc = fma(A[k * N + H], x[H], acc);
+      }
+      y[k] = acc;
+    }
+  } else {
 #pragma unroll
     for (int a = 0; a < N; ++a) {
       double acc = 0.0;
 #pragma unroll
       for (int c = 0; c < N; ++c) acc = fma(A[a * N + c], x[c], acc);
-      dst[a * stride] = acc;
+      y[a] = acc;
     }
   }
 }
 
-// kron_pass whose input is the sum of NIN (3 or 4) buffers, ((a + b) + c) + d
-// at each node (diagonal term + the direction residuals).  Each
-// line is read completely before it is written, and lines are disjoint, so
-// out may alias any input.
-template <int N, int NIN>
-__device__ __forceinline__ void kron_pass_sum(const double (&A)[N * N], int j,
-                                               const double* in0, const double* in1,
-                                               const double* in2, const double* in3, double* out,
-                                               int tid, int nthreads) {
+// One sum-factorised pass along direction j: out[.., a_j, ..] = (A x)_a over
+// each line, the input being the sum of NIN buffers ((a + b) + c) + d at each
+// node (NIN = 1: a plain pass; 3/4: diagonal term + the direction residuals).
+// A is a reference into the __grid_constant__ parameter block, so with the
+// loops unrolled every coefficient is a constant-bank operand of its DFMA (no
+// shared-memory load per multiply: 56 -> 52.5 ms at config 5).  One work item
+// per (variable, line); each line is read completely before it is written and
+// lines are disjoint, so out may alias an input.  (Splitting a line's outputs
+// over two items to fill the CTA more evenly measured slower: 58.8 ms.)
+template <int N, int MODE, int NIN = 1>
+__device__ __forceinline__ void kron_pass(const double (&A)[N * N], int j, const double* in0,
+                                          double* out, int tid, int nthreads,
+                                          const double* in1 = nullptr,
+                                          const double* in2 = nullptr,
+                                          const double* in3 = nullptr) {
   constexpr int NN = N * N * N;
   const int stride = j == 0 ? 1 : (j == 1 ? N : N * N);
   for (int t = tid; t < 5 * N * N; t += nthreads) {
@@ -127,20 +160,20 @@ __device__ __forceinline__ void kron_pass_sum(const double (&A)[N * N], int j,
     else if (j == 1) base = u0 + u1 * N * N;
     else base = u0 + u1 * N;
     const int o = v * NN + base;
-    double x[N];
+    double x[N], y[N];
 #pragma unroll
     for (int c = 0; c < N; ++c) {
       const int k = o + c * stride;
-      x[c] = (in0[k] + in1[k]) + in2[k];
-      if (NIN == 4) x[c] = x[c] + in3[k];
+      if constexpr (NIN == 1) {
+        x[c] = in0[k];
+      } else {
+        x[c] = (in0[k] + in1[k]) + in2[k];
+        if constexpr (NIN == 4) x[c] = x[c] + in3[k];
+      }
     }
+    apply_line<N, MODE>(A, x, y);
 #pragma unroll
-    for (int a = 0; a < N; ++a) {
-      double acc = 0.0;
-#pragma unroll
-      for (int c = 0; c < N; ++c) acc = fma(A[a * N + c], x[c], acc);
-      out[o + a * stride] = acc;
-    }
+    for (int a = 0; a < N; ++a) out[o + a * stride] = y[a];
   }
 }
 
@@ -208,7 +241,7 @@ struct ModalPairs {
 template <int N>
 constexpr int kModalBatch = (N >= 7) ? 1 : (N == 6 ? SFB_MODAL_BATCH_N6 : (N >= 4 ? 2 : 1));
 
-template <int N>
+template <int N, bool EO>
 __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks)
     euler_modal_kernel(int64_t E, const __grid_constant__ ModalOps<N> ops, double gm1, double c_gamma,
                        double gam_ratio, const double* __restrict__ Uhat,
@@ -275,11 +308,12 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
     }
 
     // ---- stage A: u = V^3 Uhat ------------------------------------------------
-    kron_pass<N>(sV, 0, in, res, tid, T);
+    constexpr int MV = EO ? 1 : 0, MP = EO ? 2 : 0;
+    kron_pass<N, MV>(sV, 0, in, res, tid, T);
     __syncthreads();
-    kron_pass<N>(sV, 1, res, in, tid, T);
+    kron_pass<N, MV>(sV, 1, res, in, tid, T);
     __syncthreads();
-    kron_pass<N>(sV, 2, in, res, tid, T);  // u in res
+    kron_pass<N, MV>(sV, 2, in, res, tid, T);  // u in res
     __syncthreads();
 
     // ---- stage B: node records + diagonal term ----------------------------------
@@ -401,13 +435,13 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
 
     // ---- stage D: Rhat = Pi^3 r, store, sum of squares -------------------------
     if (SFB_MODAL_COMPACT)  // r = (diag + x2) + x0 + x1
-      kron_pass_sum<N, 3>(sP, 0, res, in, dbuf1, nullptr, res, tid, T);
+      kron_pass<N, MP, 3>(sP, 0, res, res, tid, T, in, dbuf1);
     else  // r = diag + x0 + x1 + x2
-      kron_pass_sum<N, 4>(sP, 0, res, in, dbuf1, dbuf2, res, tid, T);
+      kron_pass<N, MP, 4>(sP, 0, res, res, tid, T, in, dbuf1, dbuf2);
     __syncthreads();
-    kron_pass<N>(sP, 1, res, in, tid, T);
+    kron_pass<N, MP>(sP, 1, res, in, tid, T);
     __syncthreads();
-    kron_pass<N>(sP, 2, in, res, tid, T);  // Rhat in res
+    kron_pass<N, MP>(sP, 2, in, res, tid, T);  // Rhat in res
     __syncthreads();
     double* Rg = Rhat + e * Cfg::kU;
     double ss = 0.0;
@@ -444,20 +478,34 @@ static int launch_modal(int64_t E, const double* V, const double* Pi, const doub
     ops.P[i] = Pi[i];
   }
   for (int i = 0; i < N; ++i) ops.Dd[i] = scale * D[i * N + i];
-  static int per_sm = 0;
-  if (per_sm == 0) {
-    cudaFuncSetAttribute(euler_modal_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)Cfg::kSmem);
-    int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, euler_modal_kernel<N>, Cfg::kThreads,
-                                                  Cfg::kSmem);
-    per_sm = b > 0 ? b : 1;
+  // the parity of the operators (Legendre modes on symmetric GLL nodes)
+  double vmax = 0.0, pmax = 0.0;
+  for (int i = 0; i < N * N; ++i) {
+    vmax = fmax(vmax, fabs(V[i]));
+    pmax = fmax(pmax, fabs(Pi[i]));
   }
-  int64_t grid = (int64_t)num_sms() * per_sm;
+  bool eo = SFB_MODAL_PARITY != 0;
+  for (int i = 0; i < N && eo; ++i)
+    for (int k = 0; k < N; ++k) {
+      const double sg = (k % 2 == 0) ? 1.0 : -1.0;
+      if (fabs(V[(N - 1 - i) * N + k] - sg * V[i * N + k]) > 1e-13 * vmax ||
+          fabs(Pi[k * N + (N - 1 - i)] - sg * Pi[k * N + i]) > 1e-13 * pmax)
+        eo = false;
+    }
+  auto kern = eo ? euler_modal_kernel<N, true> : euler_modal_kernel<N, false>;
+  static int per_sm[2] = {0, 0};
+  int& ps = per_sm[eo ? 1 : 0];
+  if (ps == 0) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, Cfg::kThreads, Cfg::kSmem);
+    ps = b > 0 ? b : 1;
+  }
+  int64_t grid = (int64_t)num_sms() * ps;
   if (grid > E) grid = E;
   const double gm1 = gamma - 1.0;
-  euler_modal_kernel<N><<<(unsigned)grid, Cfg::kThreads, Cfg::kSmem, s>>>(
-      E, ops, gm1, 1.0 / (2.0 * gm1), gamma / gm1, Uhat, Ja, Rhat, sumsq);
+  kern<<<(unsigned)grid, Cfg::kThreads, Cfg::kSmem, s>>>(E, ops, gm1, 1.0 / (2.0 * gm1),
+                                                         gamma / gm1, Uhat, Ja, Rhat, sumsq);
   return check_launch("euler_volume_curvilinear_modal");
 }
 

@@ -94,3 +94,24 @@ def test_full_config5_single_gpu_sampled_and_norm():
     eu.volume_curvilinear_modal(Uh[e0:e0 + cnt].contiguous(), Ja[e0:e0 + cnt].contiguous(), n,
                                 sumsq=ss3)
     assert torch.equal(ss3, ss[e0:e0 + cnt])
+
+
+@pytest.mark.parametrize("n", [5, 6])
+def test_modal_general_operators_take_the_dense_path(n):
+    # operators without the Legendre/GLL parity (a perturbed V, Pi = V^-1) must
+    # go through the dense transforms and still match the oracle
+    from paper_2306_11665_b200 import _lib
+
+    E = 5
+    Uh = eu.generate_modal_states(E, n, seed=31)
+    Ja = eu.generate_metric(E, n, seed=32)
+    _, D, V, _ = eu.gll_operators(n)
+    Vp = np.ascontiguousarray(V + 1e-3 * np.random.default_rng(n).standard_normal(V.shape))
+    Pp = np.ascontiguousarray(np.linalg.inv(Vp))
+    out = torch.empty_like(Uh)
+    ss = torch.empty(E, dtype=torch.float64, device="cuda")
+    _lib.call("sfb_euler_volume_curvilinear_modal", E, n, Vp.ctypes.data, Pp.ctypes.data,
+              np.ascontiguousarray(D).ctypes.data, 1.4, 2.0, _lib.ptr(Uh), _lib.ptr(Ja),
+              _lib.ptr(out), _lib.ptr(ss), _lib.stream_ptr())
+    ref, ref_ss = eo.euler_volume_curvilinear_modal(Uh.cpu().numpy(), Ja.cpu().numpy(), Vp, Pp, D)
+    assert max_rel(out.cpu().numpy(), ref) <= TOL
