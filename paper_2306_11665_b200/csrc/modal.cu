@@ -43,7 +43,7 @@
 #define SFB_MODAL_COMPACT 0  // 1: 69 KB smem but one more barrier: 51.0 vs 47.9 ms
 #endif
 #ifndef SFB_MODAL_BATCH_N6
-#define SFB_MODAL_BATCH_N6 3
+#define SFB_MODAL_BATCH_N6 2
 #endif
 
 namespace sfb {
