@@ -31,6 +31,9 @@
 #ifndef SFB_WARP_OWN_MINBLOCKS_N5
 #define SFB_WARP_OWN_MINBLOCKS_N5 8
 #endif
+#ifndef SFB_WARP_SLOT
+#define SFB_WARP_SLOT 1  // next block's states by cp.async into smem (0.464 -> 0.439 ms)
+#endif
 #ifndef SFB_WARP_TABLOG
 #define SFB_WARP_TABLOG 1
 #endif
@@ -292,7 +295,12 @@ __global__ void __launch_bounds__(32, WarpCfg<N>::kMinBlocksOwn)
   const int lane = threadIdx.x;
   double* rec = smem;          // [7][S]
   double* bx2 = rec + 7 * S;   // [5][S] x2-line results
-  double* bx1 = bx2 + 5 * S;   // [5][S] x1-line results
+  double* bx1 = bx2 + 5 * S;   // [5][S] x1-line results (or, kSlot, the states slot)
+  // kSlot (SFB_WARP_SLOT, even n): the next block's states are copied into the
+  // x1 buffer's space with per-lane cp.async while the lines run, and the x1
+  // results are added into the x2 buffer instead
+  constexpr bool kSlot = SFB_WARP_SLOT && (N % 2 == 0);
+  double* slot = bx1;
   if (lane == 0) {
 #pragma unroll
     for (int i = 0; i < N; ++i) ddiag[i] = Dm.d[i * (N + 1)];
@@ -330,28 +338,57 @@ __global__ void __launch_bounds__(32, WarpCfg<N>::kMinBlocksOwn)
     pos2[a] = swz<N>(u, w, a);
   }
   const double d1 = ddiag[u], d2 = ddiag[w];
+  auto issue_slot = [&](int itn) {  // this lane's x0 line of block itn -> its slot entries
+    const int64_t wbn = g + (int64_t)itn * G;
+    const int neln = nel_of(wbn);
+    const double* ub = U + (wbn * EPW + (el < neln ? el : 0)) * 5 * NN + N * L;
+    const uint32_t sl = smem_u32(slot + el * 5 * NN + N * L);
+#pragma unroll
+    for (int v = 0; v < 5; ++v)
+#pragma unroll
+      for (int a = 0; a < N; a += 2)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sl + (v * NN + a) * 8),
+                     "l"(ub + v * NN + a)
+                     : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
 
   if (lane == 0 && niter > 0) prefetch(0);
   if (lane == 0 && niter > 1) prefetch(1);
+  if (kSlot && niter > 0) issue_slot(0);
   for (int it = 0; it < niter; ++it) {
     const int64_t wb = g + (int64_t)it * G;
     const int nel = nel_of(wb);
     if (lane == 0 && it + 2 < niter) prefetch(it + 2);
     // ---- records + diagonal term of this lane's x0 line ------------------------
-    const double* ub = U + (wb * EPW + (el < nel ? el : 0)) * 5 * NN + N * L;
     double st[5][N];
+    if constexpr (kSlot) {  // states copied into this lane's slot during the previous block
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      const double* sl = slot + el * 5 * NN + N * L;
 #pragma unroll
-    for (int v = 0; v < 5; ++v) {
-      if constexpr (N % 2 == 0) {
+      for (int v = 0; v < 5; ++v)
 #pragma unroll
         for (int a = 0; a < N; a += 2) {
-          const double2 x = ld_stream_d2(ub + v * NN + a);
+          const double2 x = *reinterpret_cast<const double2*>(sl + v * NN + a);
           st[v][a] = x.x;
           st[v][a + 1] = x.y;
         }
-      } else {
+      if (it + 1 < niter) issue_slot(it + 1);  // this lane's slot entries are consumed
+    } else {
+      const double* ub = U + (wb * EPW + (el < nel ? el : 0)) * 5 * NN + N * L;
 #pragma unroll
-        for (int a = 0; a < N; ++a) st[v][a] = __ldcs(ub + v * NN + a);
+      for (int v = 0; v < 5; ++v) {
+        if constexpr (N % 2 == 0) {
+#pragma unroll
+          for (int a = 0; a < N; a += 2) {
+            const double2 x = ld_stream_d2(ub + v * NN + a);
+            st[v][a] = x.x;
+            st[v][a + 1] = x.y;
+          }
+        } else {
+#pragma unroll
+          for (int a = 0; a < N; ++a) st[v][a] = __ldcs(ub + v * NN + a);
+        }
       }
     }
     NodeRec nr[N];
@@ -418,7 +455,20 @@ __global__ void __launch_bounds__(32, WarpCfg<N>::kMinBlocksOwn)
         }
       }
       line_pairs<N>(rl, pos1, 2 * S, 3 * S, 1 * S, Dm, gm1, acc);
-      if (act) {
+      if constexpr (kSlot) {  // x1 results added into the x2 buffer (each node once)
+        __syncwarp();
+        if (act) {
+#pragma unroll
+          for (int a = 0; a < N; ++a) {
+            double* p = bx2 + el * NN + pos1[a];
+            p[0] += acc[a][0];
+            p[2 * S] += acc[a][1];
+            p[3 * S] += acc[a][2];
+            p[S] += acc[a][3];
+            p[4 * S] += acc[a][4];
+          }
+        }
+      } else if (act) {
 #pragma unroll
         for (int a = 0; a < N; ++a) {
           double* p = bx1 + el * NN + pos1[a];
@@ -440,7 +490,8 @@ __global__ void __launch_bounds__(32, WarpCfg<N>::kMinBlocksOwn)
         double o[N];
 #pragma unroll
         for (int a = 0; a < N; ++a)
-          o[a] = (acc0[a][v] + q2[v * S + pos0[a]]) + q1[v * S + pos0[a]];
+          o[a] = kSlot ? acc0[a][v] + q2[v * S + pos0[a]]
+                       : (acc0[a][v] + q2[v * S + pos0[a]]) + q1[v * S + pos0[a]];
         if constexpr (N % 2 == 0) {
 #pragma unroll
           for (int a = 0; a < N; a += 2) st_stream_d2(out + v * NN + a, make_double2(o[a], o[a + 1]));
