@@ -82,14 +82,17 @@ __device__ __forceinline__ void load_line(const double* __restrict__ rec, const 
   }
 }
 
-// Accumulate the pairs of one line: acc[a] = sum_b D[a,b] F#(a, b).
-template <int N>
+// Accumulate the pairs of one line: acc[a] (+)= sum_b D[a,b] F#(a, b)
+// (ZERO = false: onto the values already in acc).
+template <int N, bool ZERO = true>
 __device__ __forceinline__ void line_pairs_regs(const NodeRec (&nrec)[N], const DMat<N> Dm,
                                                 double gm1, double (&acc)[N][5]) {
+  if constexpr (ZERO) {
 #pragma unroll
-  for (int a = 0; a < N; ++a)
+    for (int a = 0; a < N; ++a)
 #pragma unroll
-    for (int v = 0; v < 5; ++v) acc[a][v] = 0.0;
+      for (int v = 0; v < 5; ++v) acc[a][v] = 0.0;
+  }
   constexpr PairOrder<N> po;
   constexpr int P = PairOrder<N>::kPairs;
   constexpr int K = WarpCfg<N>::kK;
@@ -119,13 +122,13 @@ __device__ __forceinline__ void line_pairs_regs(const NodeRec (&nrec)[N], const 
   }
 }
 
-template <int N>
+template <int N, bool ZERO = true>
 __device__ __forceinline__ void line_pairs(const double* __restrict__ rec, const int (&pos)[N],
                                            int vp0, int vp1, int vp2, const DMat<N> Dm, double gm1,
                                            double (&acc)[N][5]) {
   NodeRec nrec[N];
   load_line<N>(rec, pos, vp0, vp1, vp2, nrec);
-  line_pairs_regs<N>(nrec, Dm, gm1, acc);
+  line_pairs_regs<N, ZERO>(nrec, Dm, gm1, acc);
 }
 
 template <int N>
@@ -283,7 +286,8 @@ __global__ void __launch_bounds__(32, WarpCfg<N>::kMinBlocks)
 // the lane's registers until the store, and (3) the x2 / x1 results are plain
 // stores into two buffers read once by the owning lane: 164 instead of 232
 // shared-memory accesses per lane and block, for 20 more live registers.
-// Sum order per node: ((diag + x0) + x2) + x1.
+// Sum order per node: the x0 pairs accumulate onto the diagonal term, the x1
+// pairs onto the x2 results; then (diag + x0) + (x2 + x1).
 template <int N>
 __global__ void __launch_bounds__(32, WarpCfg<N>::kMinBlocksOwn)
     euler_cart_own_kernel(int64_t E, const DMat<N> Dm, double gm1, const double* __restrict__ U,
@@ -429,15 +433,8 @@ __global__ void __launch_bounds__(32, WarpCfg<N>::kMinBlocksOwn)
       acc0[a][3] = fma(wv, m2, p * d2);
       acc0[a][4] = (et + p) * wv;
     }
-    // ---- lines along x0, from the registers -------------------------------------
-    {
-      double acc[N][5];
-      line_pairs_regs<N>(nr, Dm, gm1, acc);
-#pragma unroll
-      for (int a = 0; a < N; ++a)
-#pragma unroll
-        for (int v = 0; v < 5; ++v) acc0[a][v] = acc0[a][v] + acc[a][v];
-    }
+    // ---- lines along x0, from the registers, accumulated onto the diagonal -----
+    line_pairs_regs<N, false>(nr, Dm, gm1, acc0);
     __syncwarp();  // all records in shared memory
     // ---- lines along x2 and x1: results to their buffers (plain stores) -------
     {
@@ -454,29 +451,41 @@ __global__ void __launch_bounds__(32, WarpCfg<N>::kMinBlocksOwn)
           p[4 * S] = acc[a][4];
         }
       }
-      line_pairs<N>(rl, pos1, 2 * S, 3 * S, 1 * S, Dm, gm1, acc);
-      if constexpr (kSlot) {  // x1 results added into the x2 buffer (each node once)
+      if constexpr (kSlot) {  // x1 pairs accumulated onto the x2 results of their nodes
         __syncwarp();
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+          const double* p = bx2 + el * NN + pos1[a];
+          acc[a][0] = p[0];
+          acc[a][1] = p[2 * S];
+          acc[a][2] = p[3 * S];
+          acc[a][3] = p[S];
+          acc[a][4] = p[4 * S];
+        }
+        line_pairs<N, false>(rl, pos1, 2 * S, 3 * S, 1 * S, Dm, gm1, acc);
         if (act) {
 #pragma unroll
           for (int a = 0; a < N; ++a) {
             double* p = bx2 + el * NN + pos1[a];
-            p[0] += acc[a][0];
-            p[2 * S] += acc[a][1];
-            p[3 * S] += acc[a][2];
-            p[S] += acc[a][3];
-            p[4 * S] += acc[a][4];
+            p[0] = acc[a][0];
+            p[2 * S] = acc[a][1];
+            p[3 * S] = acc[a][2];
+            p[S] = acc[a][3];
+            p[4 * S] = acc[a][4];
           }
         }
-      } else if (act) {
+      } else {  // x1 results into their own buffer
+        line_pairs<N>(rl, pos1, 2 * S, 3 * S, 1 * S, Dm, gm1, acc);
+        if (act) {
 #pragma unroll
-        for (int a = 0; a < N; ++a) {
-          double* p = bx1 + el * NN + pos1[a];
-          p[0] = acc[a][0];
-          p[2 * S] = acc[a][1];
-          p[3 * S] = acc[a][2];
-          p[S] = acc[a][3];
-          p[4 * S] = acc[a][4];
+          for (int a = 0; a < N; ++a) {
+            double* p = bx1 + el * NN + pos1[a];
+            p[0] = acc[a][0];
+            p[2 * S] = acc[a][1];
+            p[3 * S] = acc[a][2];
+            p[S] = acc[a][3];
+            p[4 * S] = acc[a][4];
+          }
         }
       }
     }
