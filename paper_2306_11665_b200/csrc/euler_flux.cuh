@@ -75,13 +75,13 @@ __device__ __forceinline__ double log_half(double x) {
   return dsel(ok, res, __longlong_as_double(0x7ff8000000000000ll));
 }
 
-// Table-driven ln(x)/2 for the n = 4 warp kernel's node records (~12 FP64
+// Table-driven ln(x)/2 for the warp kernels' node records (~10 FP64
 // operations instead of log_half's ~22 and no reciprocal): after the same
 // reduction x = 2^e m, m in [sqrt(1/2), sqrt(2)), the top mantissa bits pick
-// c ~ 1/m from a 129-entry table (tools/gen_log_table.py; c = 1 next to
-// m = 1), r = m c - 1 is formed by one FMA (|r| <= 2^-7), and
-// ln(x)/2 = e ln2/2 + (-ln c)/2 + log1p(r)/2 with the series to r^8
-// (truncation < 1e-20).  Absolute error ~1e-17 (the log mean only uses
+// c ~ 1/m from a 257-entry table (tools/gen_log_table.py; c = 1 next to
+// m = 1), r = m c - 1 is formed by one FMA (|r| <= 2^-8), and
+// ln(x)/2 = e ln2/2 + (-ln c)/2 + log1p(r)/2 with the series to r^6
+// (truncation < 2e-18).  Absolute error ~1e-17 (the log mean only uses
 // differences of these).  Non-positive / non-finite / subnormal -> NaN.
 static __device__ __align__(16) const double kLogTab[2 * SFB_LOG_TABLE_N] = {SFB_LOG_TABLE_VALUES};
 __device__ __forceinline__ double log_half_tab(double x) {
@@ -92,15 +92,13 @@ __device__ __forceinline__ double log_half_tab(double x) {
   const bool big = mh > 0x3ff6a09e;  // m > sqrt(2)
   mh = big ? mh - 0x00100000 : mh;
   e = big ? e + 1 : e;
-  int idx = (mh - SFB_LOG_TABLE_BASE) >> 13;
+  int idx = (mh - SFB_LOG_TABLE_BASE) >> SFB_LOG_TABLE_SHIFT;
   idx = min(max(idx, 0), SFB_LOG_TABLE_N - 1);
   const double2 t = __ldg(reinterpret_cast<const double2*>(kLogTab) + idx);
   const double rh = fma(__hiloint2double(mh, lo), 0.5 * t.x, -0.5);  // r/2, one rounding
   const double r2 = rh * rh;
-  // log1p(2 rh)/2 = rh - rh^2 + 4/3 rh^3 - 2 rh^4 + 16/5 rh^5 - 16/3 rh^6 + 64/7 rh^7 - 16 rh^8
-  double p = fma(rh, -16.0, 64.0 / 7.0);
-  p = fma(rh, p, -16.0 / 3.0);
-  p = fma(rh, p, 16.0 / 5.0);
+  // log1p(2 rh)/2 = rh - rh^2 + 4/3 rh^3 - 2 rh^4 + 16/5 rh^5 - 16/3 rh^6
+  double p = fma(rh, -16.0 / 3.0, 16.0 / 5.0);
   p = fma(rh, p, -2.0);
   p = fma(rh, p, 4.0 / 3.0);
   p = fma(rh, p, -1.0);
