@@ -103,8 +103,10 @@ __device__ __forceinline__ double log_half_tab(double x) {
   p = fma(rh, p, 4.0 / 3.0);
   p = fma(rh, p, -1.0);
   const double l1p = fma(r2, p, rh);
-  const double de = (double)e;
-  const double res = fma(de, kLogPolyHalf[9], fma(de, kLogPolyHalf[10], l1p + t.y));
+  // e ln2/2 with ln2/2 rounded to one double: the log mean only uses differences
+  // of these logs, in which the rounding of ln2/2 cancels exactly for equal
+  // exponents and contributes ~1e-17 per unit of exponent difference otherwise
+  const double res = fma((double)e, 3.46573590279972654709e-01, l1p + t.y);
   return dsel(ok, res, __longlong_as_double(0x7ff8000000000000ll));
 }
 
