@@ -31,6 +31,9 @@
 #ifndef SFB_WARP_OWN_MINBLOCKS_N5
 #define SFB_WARP_OWN_MINBLOCKS_N5 8
 #endif
+#ifndef SFB_WARP_PFD
+#define SFB_WARP_PFD 3  // L2 prefetch distance in blocks (3: -2% vs 2, A/B on one box)
+#endif
 #ifndef SFB_WARP_SLOT
 #define SFB_WARP_SLOT 1  // next block's states by cp.async into smem (0.464 -> 0.439 ms)
 #endif
@@ -357,13 +360,13 @@ __global__ void __launch_bounds__(32, WarpCfg<N>::kMinBlocksOwn)
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 
-  if (lane == 0 && niter > 0) prefetch(0);
-  if (lane == 0 && niter > 1) prefetch(1);
+  if (lane == 0)
+    for (int k = 0; k < SFB_WARP_PFD && k < niter; ++k) prefetch(k);
   if (kSlot && niter > 0) issue_slot(0);
   for (int it = 0; it < niter; ++it) {
     const int64_t wb = g + (int64_t)it * G;
     const int nel = nel_of(wb);
-    if (lane == 0 && it + 2 < niter) prefetch(it + 2);
+    if (lane == 0 && it + SFB_WARP_PFD < niter) prefetch(it + SFB_WARP_PFD);
     // ---- records + diagonal term of this lane's x0 line ------------------------
     double st[5][N];
     if constexpr (kSlot) {  // states copied into this lane's slot during the previous block
