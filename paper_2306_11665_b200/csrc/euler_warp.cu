@@ -351,6 +351,9 @@ __global__ void __launch_bounds__(32, WarpCfg<N>::kMinBlocksOwn)
     pos2[a] = swz<N>(u, w, a);
   }
   const double d1 = ddiag[u], d2 = ddiag[w];
+  // slot chunks (16 B) of lanes with bit 2 of L set are stored swapped, so the
+  // 16-B slot reads of a warp hit every bank group equally (conflict-free)
+  const int csw = (N % 4 == 0) ? 2 * ((L >> 2) & 1) : 0;
   auto issue_slot = [&](int itn) {  // this lane's x0 line of block itn -> its slot entries
     const int64_t wbn = g + (int64_t)itn * G;
     const int neln = nel_of(wbn);
@@ -360,7 +363,7 @@ __global__ void __launch_bounds__(32, WarpCfg<N>::kMinBlocksOwn)
     for (int v = 0; v < 5; ++v)
 #pragma unroll
       for (int a = 0; a < N; a += 2)
-        asm volatile(SFB_WARP_CPASYNC " [%0], [%1], 16;" ::"r"(sl + (v * NN + a) * 8),
+        asm volatile(SFB_WARP_CPASYNC " [%0], [%1], 16;" ::"r"(sl + (v * NN + (a ^ csw)) * 8),
                      "l"(ub + v * NN + a)
                      : "memory");
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -382,7 +385,7 @@ __global__ void __launch_bounds__(32, WarpCfg<N>::kMinBlocksOwn)
       for (int v = 0; v < 5; ++v)
 #pragma unroll
         for (int a = 0; a < N; a += 2) {
-          const double2 x = *reinterpret_cast<const double2*>(sl + v * NN + a);
+          const double2 x = *reinterpret_cast<const double2*>(sl + v * NN + (a ^ csw));
           st[v][a] = x.x;
           st[v][a + 1] = x.y;
         }
