@@ -83,9 +83,6 @@
 #ifndef SFB_WARP_SMALL
 #define SFB_WARP_SMALL 1  // 1: n = 2, 3 on the warp-autonomous kernel; 2: n = 5 too
 #endif
-#ifndef SFB_FUSED_N4
-#define SFB_FUSED_N4 1
-#endif
 #ifndef SFB_RECS_IN_REGS
 #define SFB_RECS_IN_REGS 1
 #endif
@@ -435,8 +432,6 @@ static int launch_euler_cartesian(int64_t E, const double* Dh, double gamma, dou
   return check_launch("euler_volume_cartesian");
 }
 
-int launch_euler_cart4_fused(int64_t E, const double* Dh, double gamma, double scale,
-                             const double* U, double* R, cudaStream_t s);
 
 template <int N>
 int launch_euler_cart_warp(int64_t E, const double* Dh, double gamma, double scale,
@@ -453,7 +448,6 @@ int euler_cartesian_dispatch(int64_t E, int64_t n, const double* D_host, double 
                             : launch_euler_cartesian<3>(E, D_host, gamma, scale, U, R, s);
     case 4:
       if (SFB_WARP_N4) return launch_euler_cart_warp<4>(E, D_host, gamma, scale, U, R, s);
-      if (SFB_FUSED_N4) return launch_euler_cart4_fused(E, D_host, gamma, scale, U, R, s);
       return launch_euler_cartesian<4>(E, D_host, gamma, scale, U, R, s);
     case 5:  // warp kernel (25 of 32 lanes) measured 0.98 vs 0.84 ms: CTA kernel
       return SFB_WARP_SMALL > 1 ? launch_euler_cart_warp<5>(E, D_host, gamma, scale, U, R, s)

@@ -29,10 +29,9 @@ namespace sfb {
 struct NodeRec {
   double hr;             // rho / 2
   double hv0, hv1, hv2;  // v / 2
-  double hb;             // (gamma-1) beta for chandrashekar_cart_v2 / the modal flux;
-                         // beta / 2 for chandrashekar_cart_k (euler_fused.cu)
+  double hb;             // (gamma-1) beta (see chandrashekar_cart_v2)
   double hlr;            // ln(rho) / 2
-  double hlb;            // ln(hb) / 2 (v2) or ln(beta) / 2 (cart_k): only differences are used
+  double hlb;            // ln(hb) / 2 (only differences of the logs are used)
 };
 
 // Coefficients of ln(m)/2 = atanh(f) = f + f^3 (1/3 + f^2/5 + ...), f = (m-1)/(m+1),
@@ -135,11 +134,18 @@ __device__ __forceinline__ void logmean_parts(double hx, double hy, double hlx, 
   den = dsel(series, fma(d2, -4.0 / 15.0, s2), __dsub_rn(hly, hlx));
 }
 
-// Cartesian flux for K pairs on records whose beta entries are pre-scaled by
-// 1/c_gamma = 2 (gamma - 1) (hb = (gamma - 1) beta, hlb = ln(hb)/2): the log
-// mean then returns beta_ln / c_gamma, so its reciprocal is already
-// c_gamma / beta_ln, and betabar carries the same factor, absorbed into the
-// p_hat constant (gm1 = gamma - 1): p_hat = rhobar / (2 betabar) = gm1 rhobar / sb.
+// Cartesian Chandrashekar flux for K independent pairs at once, in the
+// direction-rotated frame: the callers load the velocity components permuted
+// so that hv0 is the component along the line's direction (and write the
+// momentum results back un-permuted by address), so the flux never branches
+// or selects on the direction.  Every statement is written across the K pairs
+// so the instruction stream carries K independent dependency chains (DFMA
+// latency ~9 cycles; tools/peaks/fp64_latency.cu).
+// Records carry hb = (gamma - 1) beta and hlb = ln(hb)/2: the beta log mean
+// then returns beta_ln / c_gamma (c_gamma = 1/(2(gamma-1))), so its reciprocal
+// is already c_gamma / beta_ln, and betabar carries the same factor, absorbed
+// into the p_hat constant (gm1 = gamma - 1): p_hat = rhobar / (2 betabar) =
+// gm1 rhobar / sb.
 template <int K>
 __device__ __forceinline__ void chandrashekar_cart_v2(const NodeRec* const (&A)[K],
                                                       const NodeRec* const (&B)[K], double gm1,

@@ -1,7 +1,7 @@
 // K3, warp-autonomous (n = 2..5; the default for n = 2, 3, 4): every warp owns a private pipeline over a
 // block of EPW = floor(32 / n^2) elements and never waits on another warp.
 //
-// Why: the CTA-wide variants (euler.cu, euler_fused.cu) map one thread to one
+// Why: the CTA-wide kernel (euler.cu; a fused-role variant measured 0.587 ms) maps one thread to one
 // line, so a CTA has 3/n as many threads as nodes and the per-node stages
 // (records, store) split unevenly over its warps; at n = 4 ncu put ~26% of
 // warp samples on the CTA barriers around them.  Here one lane owns one line
