@@ -89,3 +89,29 @@ def test_rk4_arguments():
         bg.integrate_rk4(u0, 2, 5, 1e-3, -1)
     u, ent, mass = bg.integrate_rk4(u0, 2, 5, 1e-3, 0, every=1)
     assert torch.equal(u, u0) and ent.shape == (2, 1)
+
+
+def test_acceptance_entropy_and_mass_conservation():
+    # the reference's acceptance 6 (pkg/tests/test_acceptance.py:183-216) on the
+    # device path: EC flux |dS/dt| <= 1e-12 (1 + |S|) and mass conservation on
+    # 108 random states over d in {1,2,3}, n in {3..6}; the average flux breaks
+    # entropy conservation on >= 95% of them
+    rng = np.random.default_rng(66)
+    states = broken = 0
+    worst_ec = worst_mass = 0.0
+    for d in (1, 2, 3):
+        for n in (3, 4, 5, 6):
+            omega = sf.tensor_product_weights(sf.gauss_lobatto_legendre(n).weights, d)
+            u = rng.uniform(-1.0, 1.0, (9, n**d))
+            ut = torch.from_numpy(u).cuda()
+            ec = bg.time_derivative_batched(ut, d, n).cpu().numpy()
+            avg = bg.time_derivative_batched(ut, d, n, sf.average_flux).cpu().numpy()
+            for k in range(9):
+                s = 0.5 * np.dot(omega, u[k] * u[k])
+                worst_ec = max(worst_ec, abs(np.dot(omega * u[k], ec[k])) / (1.0 + abs(s)))
+                worst_mass = max(worst_mass, abs(float(np.dot(omega, ec[k]))))
+                broken += abs(np.dot(omega * u[k], avg[k])) > 1e-6
+                states += 1
+    assert states == 108
+    assert worst_ec <= 1e-12 and worst_mass <= 1e-12
+    assert broken >= 0.95 * states
