@@ -31,7 +31,16 @@
 #include "euler_flux.cuh"
 
 #ifndef SFB_MODAL_MINBLOCKS_N6
-#define SFB_MODAL_MINBLOCKS_N6 2
+#define SFB_MODAL_MINBLOCKS_N6 3
+#endif
+#ifndef SFB_MODAL_LEAN
+#define SFB_MODAL_LEAN 1  // register-lean line loop (3 CTAs/SM at n = 6)
+#endif
+#ifndef SFB_MODAL_LEAN_K
+#define SFB_MODAL_LEAN_K 1
+#endif
+#ifndef SFB_MODAL_CAP_CTAS
+#define SFB_MODAL_CAP_CTAS 0  // experiments: cap the CTAs per SM
 #endif
 #ifndef SFB_MODAL_PARITY
 #define SFB_MODAL_PARITY 1  // even/odd transforms when the operators have the parity
@@ -40,7 +49,7 @@
 #define SFB_MODAL_TABLOG 0  // table log measured 47.6 vs 47.0 ms here
 #endif
 #ifndef SFB_MODAL_COMPACT
-#define SFB_MODAL_COMPACT 0  // 1: 69 KB smem but one more barrier: 51.0 vs 47.9 ms
+#define SFB_MODAL_COMPACT 1  // 69 KB smem (3 CTAs/SM with the lean line loop: 43.3 -> 41.5 ms)
 #endif
 #ifndef SFB_MODAL_BATCH_N6
 #define SFB_MODAL_BATCH_N6 2
@@ -218,6 +227,60 @@ __device__ __forceinline__ void chandrashekar_curv_k(const NodeRec (&A)[K],
   }
 }
 
+// Register-lean pair loop for one line (SFB_MODAL_LEAN): node a is loaded once
+// per outer step, the nodes b > a are reloaded for each pair with volatile
+// shared loads (so the compiler cannot keep all n records of the line live),
+// which keeps the line stage under ~170 registers for 3 CTAs per SM.
+__device__ __forceinline__ double vlds(const double* p) {
+  double x;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(smem_u32(p)));
+  return x;
+}
+template <int NN>
+__device__ __forceinline__ void vload_node(const double* rec, const double* jd, int k, NodeRec& q,
+                                           double& jx, double& jy, double& jz) {
+  q.hr = vlds(rec + k);
+  q.hv0 = vlds(rec + NN + k);
+  q.hv1 = vlds(rec + 2 * NN + k);
+  q.hv2 = vlds(rec + 3 * NN + k);
+  q.hb = vlds(rec + 4 * NN + k);
+  q.hlr = vlds(rec + 5 * NN + k);
+  q.hlb = vlds(rec + 6 * NN + k);
+  jx = vlds(jd + k);
+  jy = vlds(jd + NN + k);
+  jz = vlds(jd + 2 * NN + k);
+}
+template <int N, int KB>
+__device__ __forceinline__ void lean_batch(const double* rec, const double* jd, int base, int stride,
+                                           int a, int b0, const NodeRec& qa, double ax, double ay,
+                                           double az, const double (&Dm)[N * N], double gm1,
+                                           double (&acc)[N][5]) {
+  constexpr int NN = N * N * N;
+  NodeRec A[KB], B[KB];
+  double nx[KB], ny[KB], nz[KB];
+#pragma unroll
+  for (int k = 0; k < KB; ++k) {
+    double bx, by, bz;
+    vload_node<NN>(rec, jd, base + (b0 + k) * stride, B[k], bx, by, bz);
+    A[k] = qa;
+    nx[k] = ax + bx;
+    ny[k] = ay + by;
+    nz[k] = az + bz;
+  }
+  double f[KB][5];
+  chandrashekar_curv_k<KB>(A, B, nx, ny, nz, gm1, f);
+#pragma unroll
+  for (int k = 0; k < KB; ++k) {
+    const int b = b0 + k;
+    const double dab = Dm[a * N + b], dba = Dm[b * N + a];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      acc[a][v] = fma(dab, f[k][v], acc[a][v]);
+      acc[b][v] = fma(dba, f[k][v], acc[b][v]);
+    }
+  }
+}
+
 template <int N>
 struct ModalPairs {
   static constexpr int kPairs = N * (N - 1) / 2;
@@ -368,7 +431,22 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
       for (int a = 0; a < N; ++a)
 #pragma unroll
         for (int v = 0; v < 5; ++v) acc[a][v] = 0.0;
-      if (active) {
+      if (SFB_MODAL_LEAN && active) {
+        const double* jd = jin + (dir * 3) * NN;  // Ja^dir_m planes
+#pragma unroll
+        for (int a = 0; a < N - 1; ++a) {
+          NodeRec qa;
+          double ax, ay, az;
+          vload_node<NN>(rec, jd, base + a * stride, qa, ax, ay, az);
+#pragma unroll
+          for (int b0 = a + 1; b0 < N; b0 += SFB_MODAL_LEAN_K) {
+            if (SFB_MODAL_LEAN_K == 2 && b0 + 1 < N)
+              lean_batch<N, 2>(rec, jd, base, stride, a, b0, qa, ax, ay, az, ops.D, gm1, acc);
+            else
+              lean_batch<N, 1>(rec, jd, base, stride, a, b0, qa, ax, ay, az, ops.D, gm1, acc);
+          }
+        }
+      } else if (active) {
         constexpr ModalPairs<N> po;
         constexpr int P = ModalPairs<N>::kPairs;
         constexpr int K = kModalBatch<N>;
@@ -500,6 +578,7 @@ static int launch_modal(int64_t E, const double* V, const double* Pi, const doub
     int b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, Cfg::kThreads, Cfg::kSmem);
     ps = b > 0 ? b : 1;
+    if (SFB_MODAL_CAP_CTAS > 0 && ps > SFB_MODAL_CAP_CTAS) ps = SFB_MODAL_CAP_CTAS;
   }
   int64_t grid = (int64_t)num_sms() * ps;
   if (grid > E) grid = E;
