@@ -20,11 +20,13 @@
 //            diagonal term sum_i D[r_i,r_i] F#(u_r,u_r; Ja^i(r)) into the
 //            residual (consistency: F#(u,u;n) = f(u).n);
 //   stage C  thread per (direction, line): each symmetric pair once, scattered
-//            to both rows; each direction's residual into its own buffer (one
-//            barrier; the x0 buffer reuses the slot's free Uhat region);
-//   stage D  three passes of Pi, the first summing diagonal + 3 direction
-//            buffers on the fly; Rhat streamed out; per-thread squares summed
-//            in a fixed order, xor-butterfly per warp, warps in order -> sumsq[e].
+//            to both rows (register-lean loop, SFB_MODAL_LEAN); then, after a
+//            barrier, the x0 residuals into the slot's free Uhat region, the x1
+//            residuals into the record planes and the x2 residuals added into
+//            the diagonal term (SFB_MODAL_COMPACT: 69 KB, 3 CTAs per SM);
+//   stage D  three passes of Pi, the first summing the three buffers on the
+//            fly; Rhat streamed out; per-thread squares summed in a fixed
+//            order, xor-butterfly per warp, warps in order -> sumsq[e].
 // The metric averaging 1/2 is folded into D (Ft is linear in n).
 #include "bulk.cuh"
 #include "common.cuh"
