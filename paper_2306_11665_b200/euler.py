@@ -11,8 +11,8 @@ with the Chandrashekar entropy-conservative flux, batched over elements:
                                   with contravariant fluxes            (config 5)
 
 States are (E, 5, n^3) float64 ([rho, rho v, E] per element, node axis
-fastest).  All arithmetic runs in sm_100a kernels (csrc/euler.cu,
-csrc/modal.cu); there is no CPU path.
+fastest).  All arithmetic runs in sm_100a kernels (csrc/euler_warp.cu for
+n = 2, 3, 4, csrc/euler.cu for n = 5..8, csrc/modal.cu); there is no CPU path.
 """
 
 import numpy as np
@@ -81,9 +81,16 @@ def volume_cartesian_host(U, n, D=None, gamma=GAMMA, scale=2.0, out=None):
     _lib.require_cuda()
     D = _host_matrix(gll_operators(n)[1] if D is None else D, n)
     if isinstance(U, torch.Tensor):
+        if U.is_cuda or U.dtype != torch.float64 or not U.is_contiguous():
+            raise ValueError("U must be a contiguous float64 host tensor (use volume_cartesian "
+                             "for device tensors)")
+        if tuple(U.shape[1:]) != (5, n**3):
+            raise ValueError(f"U must have shape (E, 5, {n**3})")
         U_ptr, E = U.data_ptr(), U.shape[0]
         if out is None:
             out = torch.empty_like(U)
+        elif out.is_cuda or out.shape != U.shape or out.dtype != torch.float64:
+            raise ValueError("out must be a float64 host tensor shaped like U")
         R_ptr = out.data_ptr()
     else:
         U = np.ascontiguousarray(U, dtype=np.float64)
