@@ -145,10 +145,17 @@ def volume_curvilinear_modal(Uhat, Ja, n, gamma=GAMMA, scale=2.0, out=None, sums
     _, D, V, Pi = gll_operators(n)
     _check_states(Uhat, n, "Uhat")
     E = Uhat.shape[0]
-    if Ja.shape != (E, 3, 3, n**3) or Ja.dtype != torch.float64 or not Ja.is_contiguous():
-        raise ValueError(f"Ja must be a contiguous float64 tensor of shape (E, 3, 3, {n**3})")
+    if (not isinstance(Ja, torch.Tensor) or not Ja.is_cuda or Ja.shape != (E, 3, 3, n**3)
+            or Ja.dtype != torch.float64 or not Ja.is_contiguous()):
+        raise ValueError(f"Ja must be a contiguous CUDA float64 tensor of shape (E, 3, 3, {n**3})")
     if out is None:
         out = torch.empty_like(Uhat)
+    else:
+        _check_states(out, n, "out")
+    if sumsq is not None and (not isinstance(sumsq, torch.Tensor) or not sumsq.is_cuda
+                              or sumsq.dtype != torch.float64 or sumsq.shape != (E,)
+                              or not sumsq.is_contiguous()):
+        raise ValueError(f"sumsq must be a contiguous CUDA float64 tensor of shape ({E},)")
     _lib.call(
         "sfb_euler_volume_curvilinear_modal", E, n, V.ctypes.data, Pi.ctypes.data, D.ctypes.data,
         float(gamma), float(scale), _lib.ptr(Uhat), _lib.ptr(Ja), _lib.ptr(out),
