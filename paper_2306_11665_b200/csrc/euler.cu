@@ -51,13 +51,13 @@
 #endif
 // per-n tuning of the CTA kernel (config-4 sweep; defaults measured best)
 #ifndef SFB_EPB_N6
-#define SFB_EPB_N6 2
+#define SFB_EPB_N6 1
 #endif
 #ifndef SFB_MB_N5
 #define SFB_MB_N5 2
 #endif
 #ifndef SFB_MB_N6
-#define SFB_MB_N6 1
+#define SFB_MB_N6 2
 #endif
 #ifndef SFB_MB_N8
 #define SFB_MB_N8 1
@@ -74,11 +74,17 @@
 #ifndef SFB_K_N8
 #define SFB_K_N8 2
 #endif
+#ifndef SFB_LEAN_N7
+#define SFB_LEAN_N7 1  // register-lean line loop: 2 CTAs/SM at n = 7 (1.47 -> 1.34 ms)
+#endif
+#ifndef SFB_LEAN_N6
+#define SFB_LEAN_N6 1  // with EPB 1 and 2 CTAs/SM: 1.115 -> 1.013 ms
+#endif
 #ifndef SFB_GENERIC_TABLOG
 #define SFB_GENERIC_TABLOG 0  // table log: +30% at n=6 (the single prep warp is latency-bound)
 #endif
 #ifndef SFB_MINBLOCKS_N7
-#define SFB_MINBLOCKS_N7 1  // 2 caps at 168 regs and spills (1.86 vs 1.54 ms at config 4)
+#define SFB_MINBLOCKS_N7 2  // with the lean line loop (without it 2 spilled: 1.86 vs 1.54 ms)
 #endif
 #ifndef SFB_WARP_SMALL
 #define SFB_WARP_SMALL 1  // 1: n = 2, 3 on the warp-autonomous kernel; 2: n = 5 too
@@ -167,6 +173,47 @@ __device__ __forceinline__ void line_work(const double* __restrict__ rec, int el
   for (int a = 0; a < N; ++a)
 #pragma unroll
     for (int v = 0; v < 5; ++v) o.acc[a][v] = 0.0;
+  if constexpr ((N == 7 && SFB_LEAN_N7) || (N == 6 && SFB_LEAN_N6)) {
+    // register-lean loop: node a once per outer step, nodes b > a re-read with
+    // volatile shared loads (no CSE keeps all n records live), so the kernel
+    // fits 168 registers and 2 CTAs per SM
+    const uint32_t rs = smem_u32(re);
+    auto vl = [&](int a, int off) {
+      double x;
+      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(rs + 8u * (uint32_t)(o.pos[a] + off)));
+      return x;
+    };
+    auto vload = [&](int a) {
+      NodeRec q;
+      q.hr = vl(a, 0);
+      q.hv0 = vl(a, o.vplane[0]);
+      q.hv1 = vl(a, o.vplane[1]);
+      q.hv2 = vl(a, o.vplane[2]);
+      q.hb = vl(a, 4 * S);
+      q.hlr = vl(a, 5 * S);
+      q.hlb = vl(a, 6 * S);
+      return q;
+    };
+#pragma unroll
+    for (int a = 0; a < N - 1; ++a) {
+      const NodeRec qa = vload(a);
+#pragma unroll
+      for (int b = a + 1; b < N; ++b) {
+        const NodeRec qb = vload(b);
+        const NodeRec* A[1] = {&qa};
+        const NodeRec* B[1] = {&qb};
+        double f[1][5];
+        chandrashekar_cart_v2<1>(A, B, gm1, f);
+        const double dab = Dm.d[a * N + b], dba = Dm.d[b * N + a];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          o.acc[a][v] = fma(dab, f[0][v], o.acc[a][v]);
+          o.acc[b][v] = fma(dba, f[0][v], o.acc[b][v]);
+        }
+      }
+    }
+    return;
+  }
   constexpr PairOrder<N> po;
   constexpr int P = PairOrder<N>::kPairs;
   constexpr int K = kPairBatch<N>;
