@@ -77,6 +77,15 @@
 #ifndef SFB_LEAN_N7
 #define SFB_LEAN_N7 1  // register-lean line loop: 2 CTAs/SM at n = 7 (1.47 -> 1.34 ms)
 #endif
+#ifndef SFB_LEAN_N5
+#define SFB_LEAN_N5 1  // 0.809 -> 0.788 ms
+#endif
+#ifndef SFB_LEAN_N8
+#define SFB_LEAN_N8 1  // 1.317 -> 1.267 ms (still 1 CTA/SM: 168 KB of shared memory)
+#endif
+#ifndef SFB_REC_SETS_N8
+#define SFB_REC_SETS_N8 2
+#endif
 #ifndef SFB_LEAN_N6
 #define SFB_LEAN_N6 1  // with EPB 1 and 2 CTAs/SM: 1.115 -> 1.013 ms
 #endif
@@ -120,7 +129,7 @@ struct EulerCartCfg {
   static constexpr int kRecVals = kPlanes * kEPB * kNodes;
   // smem (doubles): 2 input buffers + 2 record sets + 3 direction residuals + diag(D)
   static constexpr int kSlot = (kVals + 3) / 2 * 2;  // input slot: +1 double of alignment shift, kept even (16-B aligned slots)
-  static constexpr int kRecSets = (N == 4) ? SFB_REC_SETS_N4 : 2;  // record-set ring depth
+  static constexpr int kRecSets = (N == 4) ? SFB_REC_SETS_N4 : (N == 8 ? SFB_REC_SETS_N8 : 2);  // record-set ring depth
   static constexpr size_t kSmem = (size_t)(2 * kSlot + kRecSets * kRecVals + 3 * kVals + 8) * sizeof(double);
 };
 
@@ -173,7 +182,8 @@ __device__ __forceinline__ void line_work(const double* __restrict__ rec, int el
   for (int a = 0; a < N; ++a)
 #pragma unroll
     for (int v = 0; v < 5; ++v) o.acc[a][v] = 0.0;
-  if constexpr ((N == 7 && SFB_LEAN_N7) || (N == 6 && SFB_LEAN_N6)) {
+  if constexpr ((N == 7 && SFB_LEAN_N7) || (N == 6 && SFB_LEAN_N6) || (N == 8 && SFB_LEAN_N8) ||
+                (N == 5 && SFB_LEAN_N5)) {
     // register-lean loop: node a once per outer step, nodes b > a re-read with
     // volatile shared loads (no CSE keeps all n records live), so the kernel
     // fits 168 registers and 2 CTAs per SM
