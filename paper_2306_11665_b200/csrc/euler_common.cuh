@@ -21,16 +21,29 @@ __device__ __forceinline__ int swz(int r0, int r1, int r2) {
   return r2 * N * N + a + N * b;
 }
 
-// Pair order of one line: the circle-method round robin, so consecutive pairs
-// are disjoint (independent dependency chains and accumulators) - for N = 4:
-// (0,3)(1,2) (1,3)(0,2) (2,3)(0,1).
+#ifndef SFB_PAIR_LEX
+#define SFB_PAIR_LEX 1
+#endif
+// Pair order of one line.  Default: lexicographic, so a batch of K pairs
+// shares its first node (at n = 4, K = 3: (0,1)(0,2)(0,3) | (1,2)(1,3)(2,3)),
+// measured 1.5% faster than the circle-method round robin (SFB_PAIR_LEX=0:
+// consecutive pairs disjoint, e.g. (0,3)(1,2) (1,3)(0,2) (2,3)(0,1)).
 template <int N>
 struct PairOrder {
   static constexpr int kPairs = N * (N - 1) / 2;
   int a[kPairs > 0 ? kPairs : 1], b[kPairs > 0 ? kPairs : 1];
   constexpr PairOrder() : a{}, b{} {
-    const int M = (N % 2 == 0) ? N : N + 1;  // odd N: dummy node M-1
     int k = 0;
+    if (SFB_PAIR_LEX) {  // lexicographic: (0,1) (0,2) .. (0,n-1) (1,2) ..
+      for (int x = 0; x < N; ++x)
+        for (int y = x + 1; y < N; ++y) {
+          a[k] = x;
+          b[k] = y;
+          ++k;
+        }
+      return;
+    }
+    const int M = (N % 2 == 0) ? N : N + 1;  // odd N: dummy node M-1
     for (int round = 0; round < M - 1; ++round) {
       for (int i = 0; i < M / 2; ++i) {
         int x = (i == 0) ? M - 1 : (round + i) % (M - 1);
