@@ -12,7 +12,8 @@ collective; timing is the max over ranks).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--config 3|2|4|5]
 
-  --config 2   generic batched Hadamard + row sum + direction sum (n=4, 262,144 el.)
+  --config 2   generic batched Hadamard + row sum + direction sum (n=4, 262,144 el.),
+               plus the reference's sumfac-bench shape (n = 3..15) as "n_sweep"
   --config 4   config 3 swept over n = 2..8 with ~2^24 nodes each (one line, "sweep")
   --config 5   curvilinear modal Euler, n = 6, 2^21 elements sharded over the
                ranks (strong scaling) + the deterministic NCCL residual norm
@@ -390,9 +391,52 @@ def run_hadamard(args, world, rank, dev, stream, sampler, dist):
 
     ms_step, per, launches, (t0, t1) = timed_loop(step, args.steps, args.warmup, world, dist,
                                                   stream, sampler)
-    return finish_line(args, world, dev, dist, ms_step, per, launches, sampler, t0, t1,
+    line = finish_line(args, world, dev, dist, ms_step, per, launches, sampler, t0, t1,
                        units=E * 768, unit="entries/s", bytes_launch=8 * (768 + 64) * E,
                        flops_launch=2 * 768 * E, metric="FP64 Hadamard entries/s (generic batched)")
+    del F, out
+    torch.cuda.empty_cache()
+    if world == 1:
+        line["n_sweep"] = hadamard_n_sweep(dev, stream, sampler)
+    return line
+
+
+def hadamard_n_sweep(dev, stream, sampler, steps=5):
+    """The reference's own benchmark shape (sumfac-bench --dim 3 --n-min 3 --n-max 15:
+    time of the sum-factorized Hadamard region vs n, expected slope d+1 = 4) on
+    the fused batched kernel: ~2^26 Hadamard entries per point."""
+    import torch
+
+    import paper_2306_11665_b200 as sf
+    from paper_2306_11665_b200 import _lib
+    from paper_2306_11665_b200 import euler as eu
+
+    d, pts = 3, []
+    for n in range(3, 16):
+        ent = d * n ** (d + 1)
+        E = max(1, int(round(2**26 / ent)))
+        D = sf.lagrange_diff_matrix(sf.gauss_lobatto_legendre(n))
+        basis = sf.assemble_basis_factors(sf.build_sparsity_pattern(n, n, d), D, np.ones(n)).device
+        F = eu.generate_uniform(E * ent, 7, -1.0, 1.0, device=dev)
+        out = torch.empty((E, n**d), dtype=torch.float64, device=dev)
+
+        def step():
+            _lib.call("sfb_hadamard_rowsum_batched", E, n, n, d, _lib.ptr(basis), _lib.ptr(F),
+                      None, _lib.ptr(out), _lib.stream_ptr())
+
+        ms, _, _, _ = timed_loop(step, steps, 3, 1, None, stream, sampler)
+        pts.append({"n": n, "elements": E, "ms_per_step": ms, "us_per_element": ms * 1e3 / E,
+                    "entries_per_s": E * ent / (ms / 1e3),
+                    "hbm_frac": 8 * (ent + n**d) * E / (ms / 1e3) / 1e9 / measured_peaks()[0]})
+        del F, out
+        torch.cuda.empty_cache()
+    ns = np.array([p["n"] for p in pts], dtype=float)
+    t = np.array([p["us_per_element"] for p in pts])
+    return {"workload": "fused Hadamard + row sum + direction sum, d=3, n=3..15, ~2^26 entries "
+                        "per point (the reference's sumfac-bench shape, batched)",
+            "points": pts,
+            "slope_time_per_element_vs_n": float(np.polyfit(np.log(ns), np.log(t), 1)[0]),
+            "expected_slope": "d+1 = 4 (the reference's own CPU run: 3.66, BASELINE.md)"}
 
 
 def run_sweep(args, world, rank, dev, stream, sampler, dist):
@@ -504,6 +548,10 @@ def measure_other_configs(args, dev, stream, sampler, dist):
             summary["slope_time_per_dof_vs_n"] = ln["slope_time_per_dof_vs_n"]
         if cfg == 5:
             summary["residual_norm"] = ln["residual_norm"]
+        if cfg == 2 and "n_sweep" in ln:
+            summary["n_sweep_slope_time_per_element"] = ln["n_sweep"]["slope_time_per_element_vs_n"]
+            summary["n_sweep_us_per_element"] = {p["n"]: p["us_per_element"]
+                                                 for p in ln["n_sweep"]["points"]}
         out[f"config{cfg}"] = summary
         torch.cuda.empty_cache()
     out["f3_burgers_rk4"] = measure_burgers_rk4(dev)
