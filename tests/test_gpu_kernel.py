@@ -226,11 +226,14 @@ def test_config2_fused_batched_bitwise_golden():
     assert np.array_equal(out_dir.cpu().numpy(), g["out_dir"])
 
 
-@pytest.mark.parametrize("n,d", [(2, 3), (3, 3), (5, 2), (6, 3), (8, 3), (9, 2)])
+@pytest.mark.parametrize("n,d", [(2, 3), (3, 3), (5, 2), (6, 3), (8, 3), (9, 2),
+                                 (5, 3), (7, 3), (9, 3), (10, 3), (12, 3), (15, 3), (16, 3)])
 def test_fused_batched_generic_sizes_bitwise(n, d):
+    # fixed-size kernels (2|3|4|6|8, 3), (4|5, 2) and the generic kernel for
+    # the rest, up to the reference's sumfac-bench range (n <= 15) and beyond
     rng = np.random.default_rng(n * 10 + d)
     R = n ** (d - 1) * n
-    E = 37
+    E = 37 if n < 10 else 5
     basis = rng.standard_normal((d, R, n))
     F = rng.uniform(-1, 1, (E, d, R, n))
     out = torch.empty((E, R), dtype=torch.float64, device="cuda")
@@ -238,6 +241,11 @@ def test_fused_batched_generic_sizes_bitwise(n, d):
     _lib.call("sfb_hadamard_rowsum_batched", E, n, n, d, _lib.ptr(Bt), _lib.ptr(Ft), None,
               _lib.ptr(out), _lib.stream_ptr())
     assert np.array_equal(out.cpu().numpy(), (basis[None] * F).sum(axis=3).sum(axis=1))
+    # per-direction output too
+    od = torch.empty((E, d, R), dtype=torch.float64, device="cuda")
+    _lib.call("sfb_hadamard_rowsum_batched", E, n, n, d, _lib.ptr(Bt), _lib.ptr(Ft), _lib.ptr(od),
+              None, _lib.stream_ptr())
+    assert np.array_equal(od.cpu().numpy(), (basis[None] * F).sum(axis=3))
 
 
 def test_config2_full_size_sampled_and_generator():
