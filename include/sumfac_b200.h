@@ -11,9 +11,10 @@
  * numpy stage of kernel.py / burgers.py / operators.py, with the same argument
  * meaning.  Differences that follow from the device boundary:
  *
- *   - pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors), except in
- *     the *_host entry points, which take host pointers (pinned or pageable)
- *     and do the host<->device copies themselves;
+ *   - pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors), except
+ *     the small n x n operators of the Euler entries (D, V, Pi: HOST pointers,
+ *     copied into the launch parameters) and the *_host entry points, which
+ *     take host buffers (pinned or pageable) and do the copies themselves;
  *   - every call is stream-ordered on `stream` (a cudaStream_t; NULL = legacy
  *     default stream), does not synchronise, and does not allocate device
  *     memory (the *_host entry points keep one cached staging arena);
@@ -164,7 +165,8 @@ int sfb_kronecker_apply(int64_t B, int64_t d, const int64_t* rows_1d, const int6
  * with F#_j the Chandrashekar entropy-conservative two-point flux (DESIGN.md
  * "Flux"), logarithmic means by the shared series/log formula.  The volume
  * term of burgers.py:117-131 generalised to a 5-variable state; scale = 2
- * gives the 2 sum_j D o F# of BASELINE.json config 3.  n in 2..8. */
+ * gives the 2 sum_j D o F# of BASELINE.json config 3.  n in 2..8.
+ * D: HOST (n,n).  U, R: device, (E,5,n^3), 16-byte aligned. */
 int sfb_euler_volume_cartesian(int64_t E, int64_t n, const double* D, double gamma, double scale,
                                const double* U, double* R, sfb_stream_t stream);
 
@@ -179,7 +181,8 @@ int sfb_euler_volume_cartesian_host(int64_t E, int64_t n, const double* D_host, 
  *      Ft_i = sum_m 1/2 (Ja[i][m](r) + Ja[i][m](r(i->l))) F#_m
  * Rhat = (Pi x Pi x Pi) r
  * sumsq[e] = sum over v, modes of Rhat[e,v,:]^2 (deterministic order), NULL ok.
- * V, Pi, D (n,n); Uhat, Rhat (E,5,n^3); Ja (E,3,3,n^3).  n in 2..8. */
+ * V, Pi, D: HOST (n,n); Uhat, Rhat (E,5,n^3), Ja (E,3,3,n^3), sumsq (E):
+ * device, 16-byte aligned.  n in 2..8. */
 int sfb_euler_volume_curvilinear_modal(int64_t E, int64_t n, const double* V, const double* Pi,
                                        const double* D, double gamma, double scale,
                                        const double* Uhat, const double* Ja, double* Rhat,
