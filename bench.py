@@ -658,7 +658,7 @@ def main(argv=None):
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the configs 2/4/5 summaries appended to the default line")
     ap.add_argument("--cpu-sample", type=int, default=262144)
-    ap.add_argument("--cpu-seconds", type=float, default=3.0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)  # ~10-30 s of CPU work
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch of the top kernel (default: profiles/)")
     args = ap.parse_args(argv)
