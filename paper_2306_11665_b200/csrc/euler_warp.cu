@@ -38,7 +38,7 @@
 #define SFB_WARP_STCS 1  // evict-first 16-B stores (-0.9% vs L1::no_allocate)
 #endif
 #ifndef SFB_WARP_PFD
-#define SFB_WARP_PFD 3  // L2 prefetch distance in blocks (3: -2% vs 2, A/B on one box)
+#define SFB_WARP_PFD 2  // L2 prefetch distance in blocks (A/B: 2 and 3 within 0.5%)
 #endif
 #ifndef SFB_WARP_SLOT
 #define SFB_WARP_SLOT 1  // next block's states by cp.async into smem (0.464 -> 0.439 ms)
