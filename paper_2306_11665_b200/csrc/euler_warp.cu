@@ -1,30 +1,36 @@
-// K3, warp-autonomous (n = 2..5; the default for n = 2, 3, 4): every warp owns a private pipeline over a
-// block of EPW = floor(32 / n^2) elements and never waits on another warp.
+// K3, warp-autonomous (n = 2..5; the default for n = 2, 3, 4): every warp
+// owns a private pipeline over blocks of EPW = floor(32 / n^2) elements and
+// never waits on another warp.
 //
-// Why: the CTA-wide kernel (euler.cu; a fused-role variant measured 0.587 ms) maps one thread to one
-// line, so a CTA has 3/n as many threads as nodes and the per-node stages
-// (records, store) split unevenly over its warps; at n = 4 ncu put ~26% of
-// warp samples on the CTA barriers around them.  Here one lane owns one line
-// in EVERY direction (n^2 lanes per element), so each lane does exactly n
-// nodes of records, one line per direction and n nodes of store: no
-// imbalance, and __syncwarp is the only synchronisation.  (n = 2: 8 elements
-// per warp; 3: 3 elements, 27 of 32 lanes; 4: 2 elements; 5: 1 element, 25
-// lanes.  n >= 6 would need more shared memory per warp than an SM can give
-// a useful number of warps: those use euler.cu's CTA kernel.)
+// Why: the CTA-wide kernel (euler.cu) maps one thread to one line, so a CTA
+// has 3/n as many threads as nodes and the per-node stages (records, store)
+// split unevenly over its warps; at n = 4 ncu put ~26% of warp samples on the
+// CTA barriers around them.  Here one lane owns one line in EVERY direction
+// (n^2 lanes per element), so each lane does exactly n nodes of records, one
+// line per direction and n nodes of store: no imbalance, and __syncwarp is
+// the only synchronisation.  (n = 2: 8 elements per warp; 3: 3 elements, 27
+// of 32 lanes; 4: 2 elements; 5: 1 element, 25 lanes.  n >= 6 would need
+// more shared memory per warp than an SM can give a useful number of warps:
+// those use euler.cu's CTA kernel.)
 //
-// Per warp block (shared memory, 12 planes of S = EPW n^3 doubles):
+// Per warp block (shared memory, 17 planes of S = EPW n^3 doubles, 17 KB at
+// n = 4 -> 12 warps per SM with the 168 registers the kernel needs):
 //   rec   [7][S]  node records hr, hv0..2, hb, hlr, hlb (swizzled nodes;
 //                 hb = (gamma-1) beta, see chandrashekar_cart_v2)
-//   res   [5][S]  residual accumulator, seeded with the diagonal term
-// Phases: records + diagonal (states read straight from L2, where a bulk
-// prefetch issued two blocks ahead has put them); lines along x2 and x1
-// (read-modify-write res); lines along x0 add res and store straight to HBM
-// (a lane's x0 line is n contiguous doubles of every variable).
+//   bx2   [5][S]  x2-line results, then x1 pairs accumulated onto them
+//   slot  [5][S]  the next block's states (per-lane cp.async, even n; odd n
+//                 reads them straight from L2 instead and uses this space
+//                 for the x1 results)
+// Phases per block: (1) records + diagonal term of the lane's own x0 line
+// (states from the slot, the block having been prefetched to L2 two blocks
+// ahead by one bulk prefetch), then the slot refill for the next block;
+// (2) the x0 line from those registers, accumulated onto the diagonal term;
+// (3) the x2 lines from the shared records, results stored; (4) the x1 lines,
+// accumulated onto the x2 results of their nodes; (5) the owner lane adds
+// (diag + x0) + (x2 + x1) and stores its x0 line, n contiguous doubles per
+// variable (16-B evict-first stores).
 #include "euler_common.cuh"
 
-#ifndef SFB_WARP_OWN
-#define SFB_WARP_OWN 1
-#endif
 #ifndef SFB_WARP_OWN_MINBLOCKS_N4
 #define SFB_WARP_OWN_MINBLOCKS_N4 11
 #endif
@@ -46,9 +52,6 @@
 #ifndef SFB_WARP_TABLOG
 #define SFB_WARP_TABLOG 1
 #endif
-#ifndef SFB_WARP_MINBLOCKS_N4
-#define SFB_WARP_MINBLOCKS_N4 12
-#endif
 #ifndef SFB_WARP_K_N4
 #define SFB_WARP_K_N4 3
 #endif
@@ -62,11 +65,7 @@ struct WarpCfg {
   static constexpr int kEPW = 32 / kL2;       // elements per warp block
   static constexpr int kActive = kEPW * kL2;  // lanes with a line
   static constexpr int kS = kEPW * kNN;       // nodes per warp block
-  static constexpr int kVals = 12 * kS;       // rec + res
-  static constexpr size_t kSmem = (size_t)kVals * sizeof(double);
   static constexpr int kK = N == 2 ? 1 : (N == 4 ? SFB_WARP_K_N4 : (N == 3 ? 3 : 2));
-  static constexpr int kMinBlocks =
-      N == 2 ? 24 : (N == 3 ? 16 : (N == 4 ? SFB_WARP_MINBLOCKS_N4 : 12));
   static constexpr size_t kSmemOwn = (size_t)17 * kS * sizeof(double);  // rec + 2 buffers
   static constexpr int kMinBlocksOwn =
       N == 2 ? 24 : (N == 3 ? 16 : (N == 4 ? SFB_WARP_OWN_MINBLOCKS_N4 : SFB_WARP_OWN_MINBLOCKS_N5));
@@ -140,161 +139,13 @@ __device__ __forceinline__ void line_pairs(const double* __restrict__ rec, const
   line_pairs_regs<N, ZERO>(nrec, Dm, gm1, acc);
 }
 
-template <int N>
-__global__ void __launch_bounds__(32, WarpCfg<N>::kMinBlocks)
-    euler_cart_warp_kernel(int64_t E, const DMat<N> Dm, double gm1, const double* __restrict__ U,
-                           double* __restrict__ R) {
-  using Cfg = WarpCfg<N>;
-  constexpr int NN = Cfg::kNN, L2 = Cfg::kL2, EPW = Cfg::kEPW, A = Cfg::kActive, S = Cfg::kS;
-  extern __shared__ __align__(16) double smem[];
-  __shared__ double ddiag[N];
-  const int lane = threadIdx.x;
-  double* rec = smem;
-  double* res = rec + 7 * S;
-  if (lane == 0) {  // static indices: a dynamic index would copy Dm to local memory
-#pragma unroll
-    for (int i = 0; i < N; ++i) ddiag[i] = Dm.d[i * (N + 1)];
-  }
-  __syncwarp();
-
-  const int64_t nwb = (E + EPW - 1) / EPW;  // warp blocks
-  const int64_t g = blockIdx.x;
-  const int64_t G = gridDim.x;
-  const int niter = g < nwb ? (int)((nwb - 1 - g) / G) + 1 : 0;
-  auto nel_of = [&](int64_t wb) {
-    const int64_t e0 = wb * EPW;
-    return (E - e0) < EPW ? (int)(E - e0) : EPW;
-  };
-  auto prefetch = [&](int it) {  // bulk prefetch needs 16-B granules: shrink to them
-    const int64_t wb = g + (int64_t)it * G;
-    const uintptr_t b0 = (uintptr_t)(U + wb * EPW * 5 * NN);
-    const uintptr_t b1 = b0 + (uintptr_t)nel_of(wb) * 5 * NN * 8;
-    const uintptr_t a0 = (b0 + 15) & ~(uintptr_t)15, a1 = b1 & ~(uintptr_t)15;
-    if (a1 > a0)
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0))
-                   : "memory");
-  };
-
-  // this lane's line in each direction: element el, transverse (u, w); the
-  // lanes past kActive shadow lane 0's work and never write
-  const bool act = lane < A;
-  const int ln = act ? lane : 0;
-  const int el = ln / L2, L = ln - el * L2, u = L % N, w = L / N;
-  const double hgm1 = 0.5 * gm1;
-  const double* rl = rec + el * NN;
-  double* rs = res + el * NN;
-  int pos2[N], pos1[N], pos0[N];
-#pragma unroll
-  for (int a = 0; a < N; ++a) {
-    pos0[a] = swz<N>(a, u, w);
-    pos1[a] = swz<N>(u, a, w);
-    pos2[a] = swz<N>(u, w, a);
-  }
-  // D diagonal at this lane's record nodes i = ln + A j: c0, c1 are fixed per
-  // lane (A is a multiple of n^2), c2 steps with j
-  const double dd0 = ddiag[ln % N], dd1 = ddiag[(ln / N) % N];
-
-  if (lane == 0 && niter > 0) prefetch(0);
-  if (lane == 0 && niter > 1) prefetch(1);
-  for (int it = 0; it < niter; ++it) {
-    const int64_t wb = g + (int64_t)it * G;
-    const int nel = nel_of(wb);
-    if (lane == 0 && it + 2 < niter) prefetch(it + 2);
-    // ---- node records + diagonal term (N nodes per lane) ----------------------
-#pragma unroll
-    for (int j = 0; j < N; ++j) {
-      const int i = ln + A * j;
-      const int e = i / NN, r = i - e * NN;
-      const double* uu = U + (wb * EPW + (e < nel ? e : 0)) * 5 * NN + r;
-      const double rho = __ldcs(uu), m0 = __ldcs(uu + NN), m1 = __ldcs(uu + 2 * NN),
-                   m2 = __ldcs(uu + 3 * NN), et = __ldcs(uu + 4 * NN);
-      const double irho = rcp_refined(rho);
-      const double hirho = 0.5 * irho;
-      const double mm = fma(m2, m2, fma(m1, m1, m0 * m0));
-      const double X2 = fma(rho, et + et, -mm);  // 2 (rho E - |m|^2/2)
-      const double iX2 = rcp_refined(X2);
-      const double p = (hgm1 * X2) * irho;
-      const double hbeta = (rho * rho) * iX2;  // (gamma - 1) beta = rho^2 / (2X)
-      const int c0 = r % N, c1 = (r / N) % N, c2 = r / L2;
-      const int q = e * NN + swz<N>(c0, c1, c2);
-      const double lr = SFB_WARP_TABLOG ? log_half_tab(rho) : log_half(rho);
-      const double lb = SFB_WARP_TABLOG ? log_half_tab(hbeta) : log_half(hbeta);
-      // diagonal term sum_j D_{c_j c_j} f_j(u, u): with mass = D.m and
-      // w = mass / rho:  (mass, w m + p D, (E + p) w)
-      const double d0 = dd0, d1 = dd1, d2 = ddiag[c2];
-      const double mass = fma(d2, m2, fma(d1, m1, d0 * m0));
-      const double wv = mass * irho;
-      if (act) {
-        rec[q] = 0.5 * rho;
-        rec[S + q] = m0 * hirho;
-        rec[2 * S + q] = m1 * hirho;
-        rec[3 * S + q] = m2 * hirho;
-        rec[4 * S + q] = hbeta;
-        rec[5 * S + q] = lr;
-        rec[6 * S + q] = lb;
-        res[q] = mass;
-        res[S + q] = fma(wv, m0, p * d0);
-        res[2 * S + q] = fma(wv, m1, p * d1);
-        res[3 * S + q] = fma(wv, m2, p * d2);
-        res[4 * S + q] = (et + p) * wv;
-      }
-    }
-    __syncwarp();
-    double acc[N][5];
-    // ---- lines along x2, then x1: read-modify-write the accumulator -----------
-    line_pairs<N>(rl, pos2, 3 * S, 1 * S, 2 * S, Dm, gm1, acc);
-    if (act) {
-#pragma unroll
-      for (int a = 0; a < N; ++a) {
-        double* p = rs + pos2[a];
-        p[0] += acc[a][0];
-        p[3 * S] += acc[a][1];
-        p[S] += acc[a][2];
-        p[2 * S] += acc[a][3];
-        p[4 * S] += acc[a][4];
-      }
-    }
-    line_pairs<N>(rl, pos1, 2 * S, 3 * S, 1 * S, Dm, gm1, acc);
-    __syncwarp();
-    if (act) {
-#pragma unroll
-      for (int a = 0; a < N; ++a) {
-        double* p = rs + pos1[a];
-        p[0] += acc[a][0];
-        p[2 * S] += acc[a][1];
-        p[3 * S] += acc[a][2];
-        p[S] += acc[a][3];
-        p[4 * S] += acc[a][4];
-      }
-    }
-    // ---- lines along x0: finish and store (N contiguous doubles per variable) --
-    line_pairs<N>(rl, pos0, 1 * S, 2 * S, 3 * S, Dm, gm1, acc);
-    __syncwarp();
-    if (act && el < nel) {
-      double* out = R + (wb * EPW + el) * 5 * NN + N * L;
-#pragma unroll
-      for (int v = 0; v < 5; ++v) {
-        if constexpr (N % 2 == 0) {  // 16-B stores (the ABI guarantees 16-B alignment)
-#pragma unroll
-          for (int a = 0; a < N; a += 2)
-            st_stream_d2(out + v * NN + a, make_double2(rs[v * S + pos0[a]] + acc[a][v],
-                                                        rs[v * S + pos0[a + 1]] + acc[a + 1][v]));
-        } else {
-#pragma unroll
-          for (int a = 0; a < N; ++a) __stcs(out + v * NN + a, rs[v * S + pos0[a]] + acc[a][v]);
-        }
-      }
-    }
-    __syncwarp();  // rec/res are rewritten by the next block's records
-  }
-}
-
-// Variant "own line" (SFB_WARP_OWN): a lane's record nodes are the nodes of
-// its own x0 line, so (1) the x0 lines run first, straight from the records in
-// registers (no shared loads), (2) the diagonal term and the x0 result stay in
-// the lane's registers until the store, and (3) the x2 / x1 results are plain
-// stores into two buffers read once by the owning lane: 164 instead of 232
-// shared-memory accesses per lane and block, for 20 more live registers.
+// "Own line": a lane's record nodes are the nodes of its own x0 line, so (1)
+// the x0 lines run first, straight from the records in registers (no shared
+// loads), (2) the diagonal term and the x0 result stay in the lane's registers
+// until the store, and (3) the x2 / x1 results go to a buffer read once by
+// the owning lane.  (A first version gave each lane the nodes lane + 32 j and
+// read-modify-wrote a shared accumulator from every direction: 232 instead of
+// 164 shared accesses per lane and block, measured 1.6% slower.)
 // Sum order per node: the x0 pairs accumulate onto the diagonal term, the x1
 // pairs onto the x2 results; then (diag + x0) + (x2 + x1).
 template <int N>
@@ -537,9 +388,8 @@ int launch_euler_cart_warp(int64_t E, const double* Dh, double gamma, double sca
   using Cfg = WarpCfg<N>;
   DMat<N> Dm;
   for (int i = 0; i < N * N; ++i) Dm.d[i] = scale * Dh[i];
-  constexpr bool own = SFB_WARP_OWN != 0;
-  constexpr size_t smem = own ? Cfg::kSmemOwn : Cfg::kSmem;
-  auto kern = own ? euler_cart_own_kernel<N> : euler_cart_warp_kernel<N>;
+  constexpr size_t smem = Cfg::kSmemOwn;
+  auto kern = euler_cart_own_kernel<N>;
   static int per_sm = 0;
   if (per_sm == 0) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
