@@ -208,3 +208,18 @@ def test_misaligned_pointer_rejected():
     with pytest.raises(ValueError):  # 8-byte offset: not 16-byte aligned
         _lib.call("sfb_euler_volume_cartesian", E, n, Dh.ctypes.data, 1.4, 2.0,
                   _lib.ptr(U) + 8, _lib.ptr(R), _lib.stream_ptr())
+
+
+def test_beyond_int32_double_offsets():
+    # 7,000,000 elements at n = 4: U and R hold 2.24e9 doubles each, past
+    # 2^31 - element offsets must be 64-bit in every index computation
+    n, E = 4, 7_000_000
+    U = eu.generate_states(E, n, seed=77)
+    R = eu.volume_cartesian(U, n)
+    idx = np.array([0, 6_710_887, 6_710_888, E - 2, E - 1])  # around 2^31 / 320
+    _, D, _, _ = eu.gll_operators(n)
+    Us = np.concatenate([synth.euler_states(1, n, seed=77, e0=int(e)) for e in idx])
+    assert np.array_equal(U[idx].cpu().numpy(), Us)
+    assert max_rel(R[idx].cpu().numpy(), eo.euler_volume_cartesian(Us, D)) <= TOL
+    del U, R
+    torch.cuda.empty_cache()
