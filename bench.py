@@ -672,6 +672,14 @@ def main(argv=None):
         args.n = 6 if args.config == 5 else 4
     if args.elements is None:
         args.elements = 2**21 if args.config == 5 else 262144
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and argv is None:
+        # plain `python bench.py --gpus N`: relaunch as N ranks (what the driver
+        # does itself with torch.distributed.run)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", os.environ.get("MASTER_PORT", "29511"),
+               os.path.abspath(__file__), *sys.argv[1:]]
+        return subprocess.call(cmd)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
