@@ -4,6 +4,7 @@
 // overlap each other and the kernel.  One cached device staging arena per
 // process (grown on demand, never shrunk) is the only allocation the library
 // makes.
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -70,7 +71,11 @@ extern "C" int sfb_euler_volume_cartesian_host(int64_t E, int64_t n, const doubl
   const int64_t per = 5 * n * n * n;
   // ~32 MB of state per chunk: large enough to amortise the launch, small
   // enough that the pipeline fills quickly.
-  int64_t chunk = (int64_t)(4 << 20) / per;
+  int64_t chunk_doubles = (int64_t)(4 << 20);
+  // (SFB_HOST_CHUNK_MB overrides for experiments; 8/16/32/64 MB measured
+  // 16.3/15.2/14.9/15.0 ms per config-3 step)
+  if (const char* env = getenv("SFB_HOST_CHUNK_MB")) chunk_doubles = (int64_t)atoi(env) << 17;
+  int64_t chunk = chunk_doubles / per;
   if (chunk < 1) chunk = 1;
   if (chunk > E) chunk = E;
   int rc = arena_reserve((size_t)(2 * chunk * per));
