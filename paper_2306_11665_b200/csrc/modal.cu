@@ -53,6 +53,9 @@
 #ifndef SFB_MODAL_COMPACT
 #define SFB_MODAL_COMPACT 1  // 69 KB smem (3 CTAs/SM with the lean line loop: 43.3 -> 41.5 ms)
 #endif
+#ifndef SFB_MODAL_EXP_SKIP
+#define SFB_MODAL_EXP_SKIP 0  // experiments only (wrong results): skip stages A=1 B=2 C=4 D=8
+#endif
 #ifndef SFB_MODAL_BATCH_N6
 #define SFB_MODAL_BATCH_N6 2
 #endif
@@ -374,15 +377,17 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
 
     // ---- stage A: u = V^3 Uhat ------------------------------------------------
     constexpr int MV = EO ? 1 : 0, MP = EO ? 2 : 0;
+    if (!(SFB_MODAL_EXP_SKIP & 1)) {
     kron_pass<N, MV>(sV, 0, in, res, tid, T);
     __syncthreads();
     kron_pass<N, MV>(sV, 1, res, in, tid, T);
     __syncthreads();
     kron_pass<N, MV>(sV, 2, in, res, tid, T);  // u in res
     __syncthreads();
+    }
 
     // ---- stage B: node records + diagonal term ----------------------------------
-    for (int r = tid; r < NN; r += T) {
+    for (int r = tid; r < ((SFB_MODAL_EXP_SKIP & 2) ? 0 : NN); r += T) {
       const double* u = res + r;  // read this node's u, then overwrite it with its diagonal term
       const double rho = u[0], m0 = u[NN], m1 = u[2 * NN], m2 = u[3 * NN], et = u[4 * NN];
       const double irho = rcp_refined(rho);
@@ -433,7 +438,8 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
       for (int a = 0; a < N; ++a)
 #pragma unroll
         for (int v = 0; v < 5; ++v) acc[a][v] = 0.0;
-      if (SFB_MODAL_LEAN && active) {
+      if ((SFB_MODAL_EXP_SKIP & 4)) {
+      } else if (SFB_MODAL_LEAN && active) {
         const double* jd = jin + (dir * 3) * NN;  // Ja^dir_m planes
 #pragma unroll
         for (int a = 0; a < N - 1; ++a) {
@@ -514,6 +520,7 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
     }
 
     // ---- stage D: Rhat = Pi^3 r, store, sum of squares -------------------------
+    if (!(SFB_MODAL_EXP_SKIP & 8)) {
     if (SFB_MODAL_COMPACT)  // r = (diag + x2) + x0 + x1
       kron_pass<N, MP, 3>(sP, 0, res, res, tid, T, in, dbuf1);
     else  // r = diag + x0 + x1 + x2
@@ -523,6 +530,7 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
     __syncthreads();
     kron_pass<N, MP>(sP, 2, in, res, tid, T);  // Rhat in res
     __syncthreads();
+    }
     double* Rg = Rhat + e * Cfg::kU;
     double ss = 0.0;
     for (int i = tid; i < Cfg::kU; i += T) {
