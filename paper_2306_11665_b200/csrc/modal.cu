@@ -157,37 +157,67 @@ __device__ __forceinline__ void apply_line(const double (&A)[N * N], const doubl
 // per (variable, line); each line is read completely before it is written and
 // lines are disjoint, so out may alias an input.  (Splitting a line's outputs
 // over two items to fill the CTA more evenly measured slower: 58.8 ms.)
-template <int N, int MODE, int NIN = 1>
-__device__ __forceinline__ void kron_pass(const double (&A)[N * N], int j, const double* in0,
+template <int N, int MODE, int NIN = 1, int J = 0>
+__device__ __forceinline__ void kron_pass(const double (&A)[N * N], const double* in0,
                                           double* out, int tid, int nthreads,
                                           const double* in1 = nullptr,
                                           const double* in2 = nullptr,
                                           const double* in3 = nullptr) {
   constexpr int NN = N * N * N;
-  const int stride = j == 0 ? 1 : (j == 1 ? N : N * N);
+  constexpr int stride = J == 0 ? 1 : (J == 1 ? N : N * N);
+  // x0 lines are contiguous: 16-byte accesses (a stride-n line per lane with
+  // 8-byte accesses is an n-way bank conflict pattern; 48-byte strided 16-byte
+  // accesses at n = 6 cover the 32 banks once per quarter warp)
+  constexpr bool kVec = (J == 0) && (N % 2 == 0);
   for (int t = tid; t < 5 * N * N; t += nthreads) {
     const int v = t / (N * N);
     const int L = t - v * N * N;
     const int u0 = L % N, u1 = L / N;
     int base;
-    if (j == 0) base = u0 * N + u1 * N * N;
-    else if (j == 1) base = u0 + u1 * N * N;
+    if constexpr (J == 0) base = u0 * N + u1 * N * N;
+    else if constexpr (J == 1) base = u0 + u1 * N * N;
     else base = u0 + u1 * N;
     const int o = v * NN + base;
     double x[N], y[N];
+    if constexpr (kVec) {
 #pragma unroll
-    for (int c = 0; c < N; ++c) {
-      const int k = o + c * stride;
-      if constexpr (NIN == 1) {
-        x[c] = in0[k];
-      } else {
-        x[c] = (in0[k] + in1[k]) + in2[k];
-        if constexpr (NIN == 4) x[c] = x[c] + in3[k];
+      for (int c = 0; c < N; c += 2) {
+        double2 q = *reinterpret_cast<const double2*>(in0 + o + c);
+        if constexpr (NIN > 1) {
+          const double2 q1 = *reinterpret_cast<const double2*>(in1 + o + c);
+          const double2 q2 = *reinterpret_cast<const double2*>(in2 + o + c);
+          q.x = (q.x + q1.x) + q2.x;
+          q.y = (q.y + q1.y) + q2.y;
+          if constexpr (NIN == 4) {
+            const double2 q3 = *reinterpret_cast<const double2*>(in3 + o + c);
+            q.x = q.x + q3.x;
+            q.y = q.y + q3.y;
+          }
+        }
+        x[c] = q.x;
+        x[c + 1] = q.y;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        const int k = o + c * stride;
+        if constexpr (NIN == 1) {
+          x[c] = in0[k];
+        } else {
+          x[c] = (in0[k] + in1[k]) + in2[k];
+          if constexpr (NIN == 4) x[c] = x[c] + in3[k];
+        }
       }
     }
     apply_line<N, MODE>(A, x, y);
+    if constexpr (kVec) {
 #pragma unroll
-    for (int a = 0; a < N; ++a) out[o + a * stride] = y[a];
+      for (int a = 0; a < N; a += 2)
+        *reinterpret_cast<double2*>(out + o + a) = make_double2(y[a], y[a + 1]);
+    } else {
+#pragma unroll
+      for (int a = 0; a < N; ++a) out[o + a * stride] = y[a];
+    }
   }
 }
 
@@ -378,11 +408,11 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
     // ---- stage A: u = V^3 Uhat ------------------------------------------------
     constexpr int MV = EO ? 1 : 0, MP = EO ? 2 : 0;
     if (!(SFB_MODAL_EXP_SKIP & 1)) {
-    kron_pass<N, MV>(sV, 0, in, res, tid, T);
+    kron_pass<N, MV, 1, 0>(sV, in, res, tid, T);
     __syncthreads();
-    kron_pass<N, MV>(sV, 1, res, in, tid, T);
+    kron_pass<N, MV, 1, 1>(sV, res, in, tid, T);
     __syncthreads();
-    kron_pass<N, MV>(sV, 2, in, res, tid, T);  // u in res
+    kron_pass<N, MV, 1, 2>(sV, in, res, tid, T);  // u in res
     __syncthreads();
     }
 
@@ -522,13 +552,13 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
     // ---- stage D: Rhat = Pi^3 r, store, sum of squares -------------------------
     if (!(SFB_MODAL_EXP_SKIP & 8)) {
     if (SFB_MODAL_COMPACT)  // r = (diag + x2) + x0 + x1
-      kron_pass<N, MP, 3>(sP, 0, res, res, tid, T, in, dbuf1);
+      kron_pass<N, MP, 3, 0>(sP, res, res, tid, T, in, dbuf1);
     else  // r = diag + x0 + x1 + x2
-      kron_pass<N, MP, 4>(sP, 0, res, res, tid, T, in, dbuf1, dbuf2);
+      kron_pass<N, MP, 4, 0>(sP, res, res, tid, T, in, dbuf1, dbuf2);
     __syncthreads();
-    kron_pass<N, MP>(sP, 1, res, in, tid, T);
+    kron_pass<N, MP, 1, 1>(sP, res, in, tid, T);
     __syncthreads();
-    kron_pass<N, MP>(sP, 2, in, res, tid, T);  // Rhat in res
+    kron_pass<N, MP, 1, 2>(sP, in, res, tid, T);  // Rhat in res
     __syncthreads();
     }
     double* Rg = Rhat + e * Cfg::kU;
