@@ -28,17 +28,21 @@ int check_launch(const char* what) {
   return SFB_OK;
 }
 
+int current_device() {
+  int dev = 0;
+  return cudaGetDevice(&dev) == cudaSuccess && dev >= 0 ? dev : 0;
+}
+
 int num_sms() {
-  static int cached = 0;
-  if (cached == 0) {
-    int dev = 0, v = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess &&
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
-      cached = v;
-    else
-      cached = kNumSMs;
+  static std::atomic<int> cached[kMaxDevices];
+  const int dev = current_device();
+  int v = dev < kMaxDevices ? cached[dev].load(std::memory_order_relaxed) : 0;
+  if (v == 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      v = kNumSMs;
+    if (dev < kMaxDevices) cached[dev].store(v, std::memory_order_relaxed);
   }
-  return cached;
+  return v;
 }
 
 }  // namespace sfb

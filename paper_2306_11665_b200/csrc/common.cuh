@@ -9,6 +9,8 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <atomic>
 #include <string>
 
 #include "../../include/sumfac_b200.h"
@@ -20,8 +22,30 @@ int fail(int code, const std::string& msg);
 int check_launch(const char* what);
 
 constexpr int kNumSMs = 148;  // B200; only used as a grid-size hint (the
-                              // runtime value is queried once and cached).
-int num_sms();
+                              // runtime value is queried once per device and cached).
+int num_sms();  // SMs of the current device
+
+// Resident CTAs per SM of `kern` at (threads, smem) on the current device,
+// after opting the kernel in to `smem` bytes of dynamic shared memory (a
+// per-device function attribute).  Cached per device in `cache`, one slot per
+// device ordinal; concurrent first calls only repeat the same idempotent setup.
+constexpr int kMaxDevices = 64;
+using DeviceCache = std::atomic<int>[kMaxDevices];
+int current_device();
+template <typename Kern>
+int resident_ctas(Kern kern, int threads, size_t smem, DeviceCache& cache) {
+  const int dev = current_device();
+  int v = dev < kMaxDevices ? cache[dev].load(std::memory_order_relaxed) : 0;
+  if (v == 0) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, threads, smem);
+    v = b > 0 ? b : 1;
+    if (dev < kMaxDevices) cache[dev].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
 
 // ---------------------------------------------------------------------------
 // FP64 helpers

@@ -469,15 +469,8 @@ static int launch_euler_cartesian(int64_t E, const double* Dh, double gamma, dou
   using Cfg = EulerCartCfg<N>;
   DMat<N> Dm;
   for (int i = 0; i < N * N; ++i) Dm.d[i] = scale * Dh[i];
-  static int per_sm = 0;
-  if (per_sm == 0) {
-    cudaFuncSetAttribute(euler_cartesian_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)Cfg::kSmem);
-    int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, euler_cartesian_kernel<N>, Cfg::kThreads,
-                                                  Cfg::kSmem);
-    per_sm = b > 0 ? b : 1;
-  }
+  static DeviceCache cache;
+  const int per_sm = resident_ctas(euler_cartesian_kernel<N>, Cfg::kThreads, Cfg::kSmem, cache);
   const int64_t nblocks = (E + Cfg::kEPB - 1) / Cfg::kEPB;
   int64_t grid = (int64_t)num_sms() * per_sm;
   if (grid > nblocks) grid = nblocks;

@@ -390,13 +390,8 @@ int launch_euler_cart_warp(int64_t E, const double* Dh, double gamma, double sca
   for (int i = 0; i < N * N; ++i) Dm.d[i] = scale * Dh[i];
   constexpr size_t smem = Cfg::kSmemOwn;
   auto kern = euler_cart_own_kernel<N>;
-  static int per_sm = 0;
-  if (per_sm == 0) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 32, smem);
-    per_sm = b > 0 ? b : 1;
-  }
+  static DeviceCache cache;
+  const int per_sm = resident_ctas(kern, 32, smem, cache);
   const int64_t nwb = (E + Cfg::kEPW - 1) / Cfg::kEPW;
   int64_t grid = (int64_t)num_sms() * per_sm;
   if (grid > nwb) grid = nwb;

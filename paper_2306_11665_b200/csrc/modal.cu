@@ -611,15 +611,9 @@ static int launch_modal(int64_t E, const double* V, const double* Pi, const doub
         eo = false;
     }
   auto kern = eo ? euler_modal_kernel<N, true> : euler_modal_kernel<N, false>;
-  static int per_sm[2] = {0, 0};
-  int& ps = per_sm[eo ? 1 : 0];
-  if (ps == 0) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
-    int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, Cfg::kThreads, Cfg::kSmem);
-    ps = b > 0 ? b : 1;
-    if (SFB_MODAL_CAP_CTAS > 0 && ps > SFB_MODAL_CAP_CTAS) ps = SFB_MODAL_CAP_CTAS;
-  }
+  static DeviceCache cache[2];  // parity / dense kernel
+  int ps = resident_ctas(kern, Cfg::kThreads, Cfg::kSmem, cache[eo ? 1 : 0]);
+  if (SFB_MODAL_CAP_CTAS > 0 && ps > SFB_MODAL_CAP_CTAS) ps = SFB_MODAL_CAP_CTAS;
   int64_t grid = (int64_t)num_sms() * ps;
   if (grid > E) grid = E;
   const double gm1 = gamma - 1.0;
