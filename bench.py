@@ -310,7 +310,8 @@ def run_ours(args):
                            units=E * 3 * n**4, unit="entries/s",
                            bytes_launch=euler_bytes_per_element(n) * E,
                            flops_launch=euler_flops_per_element(n) * E,
-                           extra={"element_dof_per_s": None, "dof_per_element": n**3})
+                           extra={"element_dof_per_s": None, "dof_per_element": n**3},
+                           traffic=ncu_traffic(args, n, E))
         line["element_dof_per_s"] = world * E * n**3 / (line["ms_per_step"] / 1e3)
         if not args.no_e2e:  # every rank its own host buffers; max over ranks
             line["e2e"] = measure_e2e(args, U, world, dist, dev)
@@ -329,8 +330,25 @@ def run_ours(args):
     return 0
 
 
+def ncu_traffic(args, n, elements):
+    """DRAM bytes per launch of the top kernel from an ncu --set full capture of the
+    same kernel (profiles/ncu_traffic.json, per round), scaled to this launch's
+    element count; None when no capture of this config and order n exists.
+    --traffic overrides it."""
+    if args.traffic is not None:
+        return args.traffic
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            rec = json.load(f).get(f"config{args.config}")
+    except (OSError, ValueError):
+        return None
+    if not isinstance(rec, dict) or rec.get("n") != n or not rec.get("elements"):
+        return None
+    return rec["bytes"] * elements / rec["elements"]
+
+
 def finish_line(args, world, dev, dist, ms_step, per, launches, sampler, t0, t1, units, unit,
-                bytes_launch, flops_launch, extra=None, metric=METRIC):
+                bytes_launch, flops_launch, extra=None, metric=METRIC, traffic=None):
     import torch
 
     if world > 1:
@@ -352,7 +370,7 @@ def finish_line(args, world, dev, dist, ms_step, per, launches, sampler, t0, t1,
         "gpu_launches": launches,
         "clocks": sampler.summary(t0, t1),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_gbs, "unit": "GB/s",
-                     "frac": achieved / hbm_gbs, "traffic": args.traffic,
+                     "frac": achieved / hbm_gbs, "traffic": traffic,
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                      "algorithmic_bytes_per_launch": bytes_launch, "kernel_ms": kernel_ms},
         "roofline_fp64": {"achieved": achieved_tf, "peak": DFMA_MEASURED_TFLOPS,
@@ -363,7 +381,7 @@ def finish_line(args, world, dev, dist, ms_step, per, launches, sampler, t0, t1,
     if args.config == 5 or flops_launch / bytes_launch > DFMA_MEASURED_TFLOPS * 1e3 / hbm_gbs:
         # compute-bound by the algorithmic count: the FP64 roofline is the binding one
         line["roofline"], line["roofline_hbm"] = dict(line["roofline_fp64"], bound="fp64",
-                                                      traffic=args.traffic,
+                                                      traffic=traffic,
                                                       kernel_ms=kernel_ms), line["roofline"]
         del line["roofline_fp64"]
     if extra:
@@ -514,7 +532,8 @@ def run_modal(args, world, rank, dev, stream, sampler, dist):
                        units=E * n**3, unit="element-DOF/s",
                        bytes_launch=modal_bytes_per_element(n) * E,
                        flops_launch=modal_flops_per_element(n) * E,
-                       metric="FP64 element-DOF/s (3D curvilinear modal Euler flux differencing)")
+                       metric="FP64 element-DOF/s (3D curvilinear modal Euler flux differencing)",
+                       traffic=ncu_traffic(args, n, E))
     line["value"] = total * n**3 / (line["ms_per_step"] / 1e3)  # strong scaling: total DOF
     line["residual_norm"] = norm[0]
     line["hadamard_entries_per_s"] = total * 3 * n**4 / (line["ms_per_step"] / 1e3)
@@ -662,12 +681,6 @@ def main(argv=None):
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch of the top kernel (default: profiles/)")
     args = ap.parse_args(argv)
-    if args.traffic is None:
-        try:  # ncu --set full capture of the same kernel/config, summarised per round
-            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-                args.traffic = json.load(f).get(f"config{args.config}")
-        except Exception:
-            args.traffic = None
     if args.n is None:
         args.n = 6 if args.config == 5 else 4
     if args.elements is None:
