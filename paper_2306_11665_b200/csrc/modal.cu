@@ -11,8 +11,9 @@
 //
 // One persistent CTA processes one element per iteration; the next element's
 // Uhat and Ja (8.6 KB + 15.6 KB at n = 6) are prefetched with two 1-D bulk
-// copies (cp.async.bulk, UBLKCP) into the other half of a double buffer while
-// the current element is transformed, differenced and projected - all in
+// copies (cp.async.bulk, UBLKCP) into the other half of a double buffer (and
+// the one after it into L2, cp.async.bulk.prefetch) while the current
+// element is transformed, differenced and projected - all in
 // shared memory, so HBM sees exactly Uhat + Ja in and Rhat (+ 8 B) out.
 //   stage A  three sum-factorised passes of V (one per direction), thread per
 //            (variable, line), ping-ponging between the input slot and the residual buffer;
@@ -55,6 +56,9 @@
 #endif
 #ifndef SFB_MODAL_EXP_SKIP
 #define SFB_MODAL_EXP_SKIP 0  // experiments only (wrong results): skip stages A=1 B=2 C=4 D=8
+#endif
+#ifndef SFB_MODAL_L2PF
+#define SFB_MODAL_L2PF 1  // L2 prefetch one element beyond the smem copy (40.8 -> 40.5 ms)
 #endif
 #ifndef SFB_MODAL_BATCH_N6
 #define SFB_MODAL_BATCH_N6 2
@@ -383,7 +387,19 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
     bulk_g2s(dst, Uhat + e * Cfg::kU, kUB, &full[slot]);
     bulk_g2s(dst + Cfg::kU, Ja + e * Cfg::kJ, kJB, &full[slot]);
   };
-  if (kBulk && tid == 0 && (int64_t)blockIdx.x < E) issue(blockIdx.x, 0);
+  auto l2_prefetch = [&](int64_t e) {  // bytes multiple of 16 (kBulk)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Uhat + e * Cfg::kU), "r"(kUB)
+                 : "memory");
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Ja + e * Cfg::kJ), "r"(kJB)
+                 : "memory");
+  };
+  if (kBulk && tid == 0 && (int64_t)blockIdx.x < E) {
+    issue(blockIdx.x, 0);
+    for (int k = 1; k <= SFB_MODAL_L2PF; ++k) {
+      const int64_t ep = blockIdx.x + (int64_t)k * gridDim.x;
+      if (ep < E) l2_prefetch(ep);
+    }
+  }
   uint32_t parity[2] = {0, 0};
 
   int it = 0;
@@ -398,6 +414,8 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
       if (tid == 0 && nxt < E) {
         fence_proxy_async_smem();
         issue(nxt, slot ^ 1);
+        if (SFB_MODAL_L2PF > 0 && e + (int64_t)(SFB_MODAL_L2PF + 1) * gridDim.x < E)
+          l2_prefetch(e + (int64_t)(SFB_MODAL_L2PF + 1) * gridDim.x);
       }
     } else {
       for (int i = tid; i < Cfg::kU; i += T) in[i] = __ldcs(Uhat + e * Cfg::kU + i);
