@@ -227,7 +227,8 @@ def test_config2_fused_batched_bitwise_golden():
 
 
 @pytest.mark.parametrize("n,d", [(2, 3), (3, 3), (5, 2), (6, 3), (8, 3), (9, 2),
-                                 (5, 3), (7, 3), (9, 3), (10, 3), (12, 3), (15, 3), (16, 3)])
+                                 (5, 3), (7, 3), (9, 3), (10, 3), (11, 3), (12, 3), (13, 3),
+                                 (14, 3), (15, 3), (16, 3), (11, 2), (16, 2), (10, 4), (17, 3)])
 def test_fused_batched_generic_sizes_bitwise(n, d):
     # fixed-size kernels (2|3|4|6|8, 3), (4|5, 2) and the generic kernel for
     # the rest, up to the reference's sumfac-bench range (n <= 15) and beyond
