@@ -17,7 +17,8 @@
  *     take host buffers (pinned or pageable) and do the copies themselves;
  *   - every call is stream-ordered on `stream` (a cudaStream_t; NULL = legacy
  *     default stream), does not synchronise, and does not allocate device
- *     memory (the *_host entry points keep one cached staging arena);
+ *     memory (the *_host entry points keep one cached staging arena per
+ *     device; calls on one device serialise on it);
  *   - errors: the return value is SFB_OK (0) or a nonzero SFB_E* code, and
  *     sfb_last_error() returns a thread-local message.  No C++ exception
  *     crosses the ABI.  The Python layer maps SFB_EINVAL to ValueError like the
@@ -171,7 +172,9 @@ int sfb_euler_volume_cartesian(int64_t E, int64_t n, const double* D, double gam
                                const double* U, double* R, sfb_stream_t stream);
 
 /* Same, from/to HOST buffers: pipelined H2D / kernel / D2H over element
- * chunks on internal streams; returns after R_host is complete. */
+ * chunks on internal streams of the current device; returns after R_host is
+ * complete (also on error: nothing is left in flight on the caller's buffers).
+ * Pinned buffers let both copy directions overlap the kernel. */
 int sfb_euler_volume_cartesian_host(int64_t E, int64_t n, const double* D_host, double gamma,
                                     double scale, const double* U_host, double* R_host);
 
