@@ -232,3 +232,32 @@ def test_runs_are_bitwise_reproducible(n):
     a = eu.volume_cartesian(U, n)
     b = eu.volume_cartesian(U, n)
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 6, 8])
+def test_general_operator_gamma_and_scale(n):
+    # D, gamma and scale are parameters of the ABI: a dense random operator
+    # (no GLL structure, nonzero diagonal), gamma = 5/3 and scale = -0.75
+    rng = np.random.default_rng(100 + n)
+    D = rng.standard_normal((n, n))
+    E, gamma, scale = 57, 5.0 / 3.0, -0.75
+    U = eu.generate_states(E, n, seed=60 + n, gamma=gamma)
+    R = eu.volume_cartesian(U, n, D=D, gamma=gamma, scale=scale).cpu().numpy()
+    ref = eo.euler_volume_cartesian(U.cpu().numpy(), D, gamma=gamma, scale=scale)
+    assert max_rel(R, ref) <= TOL
+
+
+def test_launch_is_ordered_on_the_callers_stream():
+    # inputs produced on a side stream, the kernel launched on that stream, the
+    # result read after that stream only: no implicit default-stream ordering
+    n, E = 4, 20000
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        U = eu.generate_states(E, n, seed=8)
+        R = torch.empty_like(U)
+        for _ in range(3):
+            eu.volume_cartesian(U, n, out=R, stream=s)
+        R2 = R * 1.0
+    s.synchronize()
+    ref = eu.volume_cartesian(U, n)
+    assert torch.equal(R2, ref)

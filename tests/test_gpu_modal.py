@@ -115,3 +115,14 @@ def test_modal_general_operators_take_the_dense_path(n):
               _lib.ptr(out), _lib.ptr(ss), _lib.stream_ptr())
     ref, ref_ss = eo.euler_volume_curvilinear_modal(Uh.cpu().numpy(), Ja.cpu().numpy(), Vp, Pp, D)
     assert max_rel(out.cpu().numpy(), ref) <= TOL
+
+
+def test_modal_gamma_and_scale():
+    n, E, gamma, scale = 4, 40, 1.3, 1.5
+    Uh = eu.generate_modal_states(E, n, seed=91)
+    Ja = eu.generate_metric(E, n, seed=92)
+    R = eu.volume_curvilinear_modal(Uh, Ja, n, gamma=gamma, scale=scale).cpu().numpy()
+    _, D, V, Pi = eu.gll_operators(n)
+    ref, _ = eo.euler_volume_curvilinear_modal(Uh.cpu().numpy(), Ja.cpu().numpy(), V, Pi, D,
+                                               gamma=gamma, scale=scale)
+    assert max_rel(R, ref) <= TOL
