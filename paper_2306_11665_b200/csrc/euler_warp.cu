@@ -29,6 +29,14 @@
 // accumulated onto the x2 results of their nodes; (5) the owner lane adds
 // (diag + x0) + (x2 + x1) and stores its x0 line, n contiguous doubles per
 // variable (16-B evict-first stores).
+// Work distribution (n = 4): one CTA of 12 such warps per SM owns a
+// contiguous range of warp blocks and its warps claim the next block from a
+// shared-memory counter, PFD + 1 blocks ahead (the prefetches need them).
+// With a static block-cyclic split over one-warp CTAs the warps the scheduler
+// favours finished after 267 us and the last after 429 us (per-warp
+// %globaltimer, tools/cta_times.py): the SM ran under-occupied for the last
+// third of the kernel (81% mean occupancy); claiming keeps all 12 warps busy
+// to the end (97%): 0.416 -> 0.400 ms.
 #include "euler_common.cuh"
 
 #ifndef SFB_WARP_OWN_MINBLOCKS_N4
@@ -48,6 +56,12 @@
 #endif
 #ifndef SFB_WARP_SLOT
 #define SFB_WARP_SLOT 1  // next block's states by cp.async into smem (0.464 -> 0.439 ms)
+#endif
+#ifndef SFB_WARP_DYN_N4
+#define SFB_WARP_DYN_N4 12  // warps per CTA at n = 4 (> 1: dynamic block claims; 0.416 -> 0.400 ms)
+#endif
+#ifndef SFB_WARP_EXP_TIMES
+#define SFB_WARP_EXP_TIMES 0
 #endif
 #ifndef SFB_WARP_TABLOG
 #define SFB_WARP_TABLOG 1
@@ -148,16 +162,23 @@ __device__ __forceinline__ void line_pairs(const double* __restrict__ rec, const
 // 164 shared accesses per lane and block, measured 1.6% slower.)
 // Sum order per node: the x0 pairs accumulate onto the diagonal term, the x1
 // pairs onto the x2 results; then (diag + x0) + (x2 + x1).
-template <int N>
-__global__ void __launch_bounds__(32, WarpCfg<N>::kMinBlocksOwn)
+template <int N, int W>
+__global__ void __launch_bounds__(32 * W, W == 1 ? WarpCfg<N>::kMinBlocksOwn : 1)
     euler_cart_own_kernel(int64_t E, const DMat<N> Dm, double gm1, const double* __restrict__ U,
                           double* __restrict__ R) {
   using Cfg = WarpCfg<N>;
   constexpr int NN = Cfg::kNN, L2 = Cfg::kL2, EPW = Cfg::kEPW, A = Cfg::kActive, S = Cfg::kS;
+  // W == 1: one warp per CTA, warp blocks g, g + G, ... (static).  W > 1: one
+  // CTA of W warps per SM owns a contiguous range of warp blocks and its warps
+  // claim them one at a time from a shared counter (dynamic), so warps the
+  // scheduler favours do not finish early and leave the SM under-occupied.
+  constexpr bool kDyn = W > 1;
   extern __shared__ __align__(16) double smem[];
   __shared__ double ddiag[N];
-  const int lane = threadIdx.x;
-  double* rec = smem;          // [7][S]
+  __shared__ unsigned int ctr;
+  const int lane = threadIdx.x & 31;
+  const int wid = kDyn ? (int)(threadIdx.x >> 5) : 0;
+  double* rec = smem + (size_t)wid * (Cfg::kSmemOwn / sizeof(double));  // [7][S]
   double* bx2 = rec + 7 * S;   // [5][S] x2-line results
   double* bx1 = bx2 + 5 * S;   // [5][S] x1-line results (or, kSlot, the states slot)
   // kSlot (SFB_WARP_SLOT, even n): the next block's states are copied into the
@@ -165,22 +186,34 @@ __global__ void __launch_bounds__(32, WarpCfg<N>::kMinBlocksOwn)
   // results are added into the x2 buffer instead
   constexpr bool kSlot = SFB_WARP_SLOT && (N % 2 == 0);
   double* slot = bx1;
-  if (lane == 0) {
+  if (threadIdx.x == 0) {
 #pragma unroll
     for (int i = 0; i < N; ++i) ddiag[i] = Dm.d[i * (N + 1)];
+    if (kDyn) ctr = 0;
   }
-  __syncwarp();
+  if (kDyn) __syncthreads();
+  else __syncwarp();
 
   const int64_t nwb = (E + EPW - 1) / EPW;
   const int64_t g = blockIdx.x;
   const int64_t G = gridDim.x;
-  const int niter = g < nwb ? (int)((nwb - 1 - g) / G) + 1 : 0;
+  const int niter = (!kDyn && g < nwb) ? (int)((nwb - 1 - g) / G) + 1 : 0;
+  // kDyn: this CTA's range [lo, hi) and the claimed blocks of iterations it .. it + PFD
+  const int64_t lo = kDyn ? nwb * g / G : 0, hi = kDyn ? nwb * (g + 1) / G : 0;
+  int64_t q[SFB_WARP_PFD + 1];
+  auto claim = [&]() -> int64_t {
+    unsigned int v = 0;
+    if (lane == 0) v = atomicAdd(&ctr, 1u);
+    return lo + (int64_t)__shfl_sync(0xffffffffu, v, 0);
+  };
+  // block of iteration it + k, and whether it exists
+  auto blk = [&](int it, int k) -> int64_t { return kDyn ? q[k] : g + (int64_t)(it + k) * G; };
+  auto has = [&](int it, int k) -> bool { return kDyn ? q[k] < hi : it + k < niter; };
   auto nel_of = [&](int64_t wb) {
     const int64_t e0 = wb * EPW;
     return (E - e0) < EPW ? (int)(E - e0) : EPW;
   };
-  auto prefetch = [&](int it) {
-    const int64_t wb = g + (int64_t)it * G;
+  auto prefetch = [&](int64_t wb) {
     const uintptr_t b0 = (uintptr_t)(U + wb * EPW * 5 * NN);
     const uintptr_t b1 = b0 + (uintptr_t)nel_of(wb) * 5 * NN * 8;
     const uintptr_t a0 = (b0 + 15) & ~(uintptr_t)15, a1 = b1 & ~(uintptr_t)15;
@@ -205,8 +238,7 @@ __global__ void __launch_bounds__(32, WarpCfg<N>::kMinBlocksOwn)
   // slot chunks (16 B) of lanes with bit 2 of L set are stored swapped, so the
   // 16-B slot reads of a warp hit every bank group equally (conflict-free)
   const int csw = (N % 4 == 0) ? 2 * ((L >> 2) & 1) : 0;
-  auto issue_slot = [&](int itn) {  // this lane's x0 line of block itn -> its slot entries
-    const int64_t wbn = g + (int64_t)itn * G;
+  auto issue_slot = [&](int64_t wbn) {  // this lane's x0 line of block wbn -> its slot entries
     const int neln = nel_of(wbn);
     const double* ub = U + (wbn * EPW + (el < neln ? el : 0)) * 5 * NN + N * L;
     const uint32_t sl = smem_u32(slot + el * 5 * NN + N * L);
@@ -220,13 +252,21 @@ __global__ void __launch_bounds__(32, WarpCfg<N>::kMinBlocksOwn)
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 
+#if SFB_WARP_EXP_TIMES
+  uint64_t t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
+  if constexpr (kDyn) {
+#pragma unroll
+    for (int k = 0; k <= SFB_WARP_PFD; ++k) q[k] = claim();
+  }
   if (lane == 0)
-    for (int k = 0; k < SFB_WARP_PFD && k < niter; ++k) prefetch(k);
-  if (kSlot && niter > 0) issue_slot(0);
-  for (int it = 0; it < niter; ++it) {
-    const int64_t wb = g + (int64_t)it * G;
+    for (int k = 0; k < SFB_WARP_PFD && has(0, k); ++k) prefetch(blk(0, k));
+  if (kSlot && has(0, 0)) issue_slot(blk(0, 0));
+  for (int it = 0; has(it, 0); ++it) {
+    const int64_t wb = blk(it, 0);
     const int nel = nel_of(wb);
-    if (lane == 0 && it + SFB_WARP_PFD < niter) prefetch(it + SFB_WARP_PFD);
+    if (lane == 0 && has(it, SFB_WARP_PFD)) prefetch(blk(it, SFB_WARP_PFD));
     // ---- records + diagonal term of this lane's x0 line ------------------------
     double st[5][N];
     if constexpr (kSlot) {  // states copied into this lane's slot during the previous block
@@ -240,7 +280,7 @@ __global__ void __launch_bounds__(32, WarpCfg<N>::kMinBlocksOwn)
           st[v][a] = x.x;
           st[v][a + 1] = x.y;
         }
-      if (it + 1 < niter) issue_slot(it + 1);  // this lane's slot entries are consumed
+      if (has(it, 1)) issue_slot(blk(it, 1));  // this lane's slot entries are consumed
     } else {
       const double* ub = U + (wb * EPW + (el < nel ? el : 0)) * 5 * NN + N * L;
 #pragma unroll
@@ -379,7 +419,24 @@ __global__ void __launch_bounds__(32, WarpCfg<N>::kMinBlocksOwn)
       }
     }
     __syncwarp();  // buffers and records are rewritten by the next block
+    if constexpr (kDyn) {
+#pragma unroll
+      for (int k = 0; k < SFB_WARP_PFD; ++k) q[k] = q[k + 1];
+      q[SFB_WARP_PFD] = claim();
+    }
   }
+#if SFB_WARP_EXP_TIMES  // experiments only: per-warp start / end times over R's first doubles
+  uint64_t t_end;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+  if (lane == 0) {
+    const unsigned gw = blockIdx.x * W + wid, GW = gridDim.x * W;
+    R[gw] = __longlong_as_double((long long)t_end);
+    R[GW + gw] = __longlong_as_double((long long)t_start);
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    R[2 * GW + gw] = __longlong_as_double((long long)smid);
+  }
+#endif
 }
 
 template <int N>
@@ -388,14 +445,16 @@ int launch_euler_cart_warp(int64_t E, const double* Dh, double gamma, double sca
   using Cfg = WarpCfg<N>;
   DMat<N> Dm;
   for (int i = 0; i < N * N; ++i) Dm.d[i] = scale * Dh[i];
-  constexpr size_t smem = Cfg::kSmemOwn;
-  auto kern = euler_cart_own_kernel<N>;
+  constexpr int W = (N == 4) ? SFB_WARP_DYN_N4 : 1;  // warps per CTA (W > 1: dynamic)
+  constexpr size_t smem = W * Cfg::kSmemOwn;
+  auto kern = euler_cart_own_kernel<N, W>;
   static DeviceCache cache;
-  const int per_sm = resident_ctas(kern, 32, smem, cache);
+  const int per_sm = resident_ctas(kern, 32 * W, smem, cache);
   const int64_t nwb = (E + Cfg::kEPW - 1) / Cfg::kEPW;
   int64_t grid = (int64_t)num_sms() * per_sm;
-  if (grid > nwb) grid = nwb;
-  kern<<<(unsigned)grid, 32, smem, s>>>(E, Dm, gamma - 1.0, U, R);
+  const int64_t need = (nwb + W - 1) / W;
+  if (grid > need) grid = need;
+  kern<<<(unsigned)grid, 32 * W, smem, s>>>(E, Dm, gamma - 1.0, U, R);
   return check_launch("euler_volume_cartesian(warp-autonomous)");
 }
 
