@@ -29,7 +29,8 @@
 // accumulated onto the x2 results of their nodes; (5) the owner lane adds
 // (diag + x0) + (x2 + x1) and stores its x0 line, n contiguous doubles per
 // variable (16-B evict-first stores).
-// Work distribution (n = 4): one CTA of 12 such warps per SM owns a
+// Work distribution: a CTA of W such warps (n = 4: 12, one CTA per SM;
+// n = 3: 8 and n = 2: 12, two per SM) owns a
 // contiguous range of warp blocks and its warps claim the next block from a
 // shared-memory counter, PFD + 1 blocks ahead (the prefetches need them).
 // With a static block-cyclic split over one-warp CTAs the warps the scheduler
@@ -59,6 +60,12 @@
 #endif
 #ifndef SFB_WARP_DYN_N4
 #define SFB_WARP_DYN_N4 12  // warps per CTA at n = 4 (> 1: dynamic block claims; 0.416 -> 0.400 ms)
+#endif
+#ifndef SFB_WARP_DYN_N3
+#define SFB_WARP_DYN_N3 8  // 2 CTAs of 8 warps per SM: 0.551 -> 0.531 ms (config-4 point)
+#endif
+#ifndef SFB_WARP_DYN_N2
+#define SFB_WARP_DYN_N2 12  // 2 CTAs of 12 warps per SM: 0.454 -> 0.422 ms
 #endif
 #ifndef SFB_WARP_EXP_TIMES
 #define SFB_WARP_EXP_TIMES 0
@@ -445,7 +452,9 @@ int launch_euler_cart_warp(int64_t E, const double* Dh, double gamma, double sca
   using Cfg = WarpCfg<N>;
   DMat<N> Dm;
   for (int i = 0; i < N * N; ++i) Dm.d[i] = scale * Dh[i];
-  constexpr int W = (N == 4) ? SFB_WARP_DYN_N4 : 1;  // warps per CTA (W > 1: dynamic)
+  constexpr int W = (N == 4) ? SFB_WARP_DYN_N4
+                   : (N == 3) ? SFB_WARP_DYN_N3
+                   : (N == 2) ? SFB_WARP_DYN_N2 : 1;  // warps per CTA (W > 1: dynamic)
   constexpr size_t smem = W * Cfg::kSmemOwn;
   auto kern = euler_cart_own_kernel<N, W>;
   static DeviceCache cache;
