@@ -632,11 +632,46 @@ def measure_e2e(args, U_dev, world=1, dist=None, dev=None):
     Rd = eu.volume_cartesian(U_dev[:1].contiguous(), n).cpu()
     assert torch.equal(Rd[0], Rh[0]), "e2e result differs from the device path"
     nbytes = Uh.numel() * 8
+    ceil_ms = pcie_ceiling_ms(Uh, Rh, U_dev)
     return {"value": world * E * 3 * n**4 / sec, "unit": "entries/s",
             "h2d_bytes_per_step": world * nbytes, "d2h_bytes_per_step": world * nbytes,
             "ms_per_step": sec * 1e3, "steps": steps, "n_ranks": world,
+            "pcie_ceiling_ms": ceil_ms, "frac_of_pcie_ceiling": ceil_ms / (sec * 1e3),
+            "pcie_ceiling": "same box, same buffers: pinned H2D of U and D2H of R as two "
+                            "concurrent plain copies (no kernel), CUDA events",
             "path": "sfb_euler_volume_cartesian_host (pinned host buffers, 3-stream "
                     "chunked H2D/kernel/D2H pipeline), wall clock per call"}
+
+
+def pcie_ceiling_ms(Uh, Rh, U_dev, reps=5):
+    """Time of the e2e step's copies alone (pinned U -> device, device -> pinned
+    R, concurrently on two streams): the link ceiling the e2e leg is read against."""
+    import torch
+
+    D = torch.empty_like(U_dev)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def both():
+        cur = torch.cuda.current_stream()
+        s1.wait_stream(cur)
+        s2.wait_stream(cur)
+        with torch.cuda.stream(s1):
+            D.copy_(Uh, non_blocking=True)
+        with torch.cuda.stream(s2):
+            Rh.copy_(U_dev, non_blocking=True)
+        cur.wait_stream(s1)
+        cur.wait_stream(s2)
+
+    both()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        both()
+    e1.record()
+    torch.cuda.synchronize()
+    del D
+    return e0.elapsed_time(e1) / reps
 
 
 def measure_cpu_baseline(args, U_dev):
