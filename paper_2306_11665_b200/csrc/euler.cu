@@ -105,6 +105,23 @@
 #define SFB_PREP_WARPS_N4 1
 #endif
 
+// n = 5..8 on the barrier-synchronised CTA kernel (euler_sync.cu) instead of
+// the warp-specialised one below; config-4 points (ms, sync vs this file's):
+// n = 5 1.00 vs 0.79, n = 6 0.95 vs 1.01, n = 7 1.46 (3 CTAs at 136 regs) /
+// 1.98 (2 CTAs) vs 1.34, n = 8 1.33 vs 1.27: only n = 6 takes it
+#ifndef SFB_SYNC_N5
+#define SFB_SYNC_N5 0
+#endif
+#ifndef SFB_SYNC_N6
+#define SFB_SYNC_N6 1
+#endif
+#ifndef SFB_SYNC_N7
+#define SFB_SYNC_N7 0
+#endif
+#ifndef SFB_SYNC_N8
+#define SFB_SYNC_N8 0
+#endif
+
 namespace sfb {
 
 template <int N>
@@ -486,6 +503,9 @@ static int launch_euler_cartesian(int64_t E, const double* Dh, double gamma, dou
 template <int N>
 int launch_euler_cart_warp(int64_t E, const double* Dh, double gamma, double scale,
                            const double* U, double* R, cudaStream_t s);
+template <int N>
+int launch_euler_cart_sync(int64_t E, const double* Dh, double gamma, double scale,
+                           const double* U, double* R, cudaStream_t s);
 
 int euler_cartesian_dispatch(int64_t E, int64_t n, const double* D_host, double gamma,
                              double scale, const double* U, double* R, cudaStream_t s) {
@@ -500,11 +520,18 @@ int euler_cartesian_dispatch(int64_t E, int64_t n, const double* D_host, double 
       if (SFB_WARP_N4) return launch_euler_cart_warp<4>(E, D_host, gamma, scale, U, R, s);
       return launch_euler_cartesian<4>(E, D_host, gamma, scale, U, R, s);
     case 5:  // warp kernel (25 of 32 lanes) measured 0.98 vs 0.84 ms: CTA kernel
+      if (SFB_SYNC_N5) return launch_euler_cart_sync<5>(E, D_host, gamma, scale, U, R, s);
       return SFB_WARP_SMALL > 1 ? launch_euler_cart_warp<5>(E, D_host, gamma, scale, U, R, s)
                                 : launch_euler_cartesian<5>(E, D_host, gamma, scale, U, R, s);
-    case 6: return launch_euler_cartesian<6>(E, D_host, gamma, scale, U, R, s);
-    case 7: return launch_euler_cartesian<7>(E, D_host, gamma, scale, U, R, s);
-    case 8: return launch_euler_cartesian<8>(E, D_host, gamma, scale, U, R, s);
+    case 6:
+      if (SFB_SYNC_N6) return launch_euler_cart_sync<6>(E, D_host, gamma, scale, U, R, s);
+      return launch_euler_cartesian<6>(E, D_host, gamma, scale, U, R, s);
+    case 7:
+      if (SFB_SYNC_N7) return launch_euler_cart_sync<7>(E, D_host, gamma, scale, U, R, s);
+      return launch_euler_cartesian<7>(E, D_host, gamma, scale, U, R, s);
+    case 8:
+      if (SFB_SYNC_N8) return launch_euler_cart_sync<8>(E, D_host, gamma, scale, U, R, s);
+      return launch_euler_cartesian<8>(E, D_host, gamma, scale, U, R, s);
     default: return fail(SFB_ENOTSUP, "euler_volume_cartesian: n must be in 2..8");
   }
 }

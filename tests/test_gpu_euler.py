@@ -122,6 +122,22 @@ def test_host_buffer_entry_matches_device_entry():
     assert np.array_equal(Rn, Rd.cpu().numpy())
 
 
+@pytest.mark.parametrize("n,E", [(4, 100003), (3, 77777), (6, 30001)])
+def test_host_entry_many_chunks(n, E, monkeypatch):
+    # a ragged last chunk, and with a small chunk size many chunks cycling
+    # through every stream of the pipeline
+    U = eu.generate_states(E, n, seed=13)
+    Rd = eu.volume_cartesian(U, n).cpu()
+    Uh = eu.pinned_empty((E, 5, n**3))
+    Uh.copy_(U.cpu())
+    for env in ({}, {"SFB_HOST_CHUNK_MB": "2"}, {"SFB_HOST_CHUNK_MB": "5"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        assert torch.equal(eu.volume_cartesian_host(Uh, n), Rd), env
+        for k in env:
+            monkeypatch.delenv(k)
+
+
 @pytest.mark.parametrize("d,n", [(1, 6), (2, 4), (3, 3), (3, 4), (3, 6), (2, 9)])
 def test_burgers_volume_residual_golden(d, n):
     g = golden("burgers.npz")

@@ -1,0 +1,7 @@
+# every build/variants/*.so: the Euler GPU parity tests, then the config-4 sweep
+for lib in build/variants/*.so; do
+  echo "== $lib"
+  SFB_LIB=$lib timeout 600 python -m pytest tests/test_gpu_euler.py -x -q 2>&1 | tail -2
+  SFB_LIB=$lib python bench.py --config 4 --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/sw4.json 2>gpurun_out/sw4.err
+  python -c "import json,sys; d=json.load(open('gpurun_out/sw4.json')); print(sys.argv[1], ' '.join('n%d:%.3f'%(p['n'],p['ms_per_step']) for p in d['sweep']))" $lib || tail -3 gpurun_out/sw4.err
+done
