@@ -29,8 +29,8 @@
 // accumulated onto the x2 results of their nodes; (5) the owner lane adds
 // (diag + x0) + (x2 + x1) and stores its x0 line, n contiguous doubles per
 // variable (16-B evict-first stores).
-// Work distribution: a CTA of W such warps (n = 4: 12, one CTA per SM;
-// n = 3: 8 and n = 2: 12, two per SM) owns a
+// Work distribution: a CTA of W such warps (n = 4 and 3: 12, n = 2: 16; one
+// CTA per SM, the register file being the limit) owns a
 // contiguous range of warp blocks and its warps claim the next block from a
 // shared-memory counter, PFD + 1 blocks ahead (the prefetches need them).
 // With a static block-cyclic split over one-warp CTAs the warps the scheduler
@@ -62,10 +62,16 @@
 #define SFB_WARP_DYN_N4 12  // warps per CTA at n = 4 (> 1: dynamic block claims; 0.416 -> 0.400 ms)
 #endif
 #ifndef SFB_WARP_DYN_N3
-#define SFB_WARP_DYN_N3 8  // 2 CTAs of 8 warps per SM: 0.551 -> 0.531 ms (config-4 point)
+#define SFB_WARP_DYN_N3 12  // one 12-warp CTA per SM (168 regs): 0.551 -> 0.523 ms (config-4 point; 8 warps 0.532)
+#endif
+#ifndef SFB_WARP_MB_N2
+#define SFB_WARP_MB_N2 1
+#endif
+#ifndef SFB_WARP_MB_N3
+#define SFB_WARP_MB_N3 1
 #endif
 #ifndef SFB_WARP_DYN_N2
-#define SFB_WARP_DYN_N2 12  // 2 CTAs of 12 warps per SM: 0.454 -> 0.422 ms
+#define SFB_WARP_DYN_N2 16  // one 16-warp CTA per SM (128 regs): 0.454 -> 0.417 ms (12 warps 0.423)
 #endif
 #ifndef SFB_WARP_EXP_TIMES
 #define SFB_WARP_EXP_TIMES 0
@@ -88,6 +94,8 @@ struct WarpCfg {
   static constexpr int kS = kEPW * kNN;       // nodes per warp block
   static constexpr int kK = N == 2 ? 1 : (N == 4 ? SFB_WARP_K_N4 : (N == 3 ? 3 : 2));
   static constexpr size_t kSmemOwn = (size_t)17 * kS * sizeof(double);  // rec + 2 buffers
+  // CTAs per SM asked of ptxas for the dynamic-claim CTAs (W > 1)
+  static constexpr int kMinBlocksDyn = N == 2 ? SFB_WARP_MB_N2 : (N == 3 ? SFB_WARP_MB_N3 : 1);
   static constexpr int kMinBlocksOwn =
       N == 2 ? 24 : (N == 3 ? 16 : (N == 4 ? SFB_WARP_OWN_MINBLOCKS_N4 : SFB_WARP_OWN_MINBLOCKS_N5));
 };
@@ -170,7 +178,7 @@ __device__ __forceinline__ void line_pairs(const double* __restrict__ rec, const
 // Sum order per node: the x0 pairs accumulate onto the diagonal term, the x1
 // pairs onto the x2 results; then (diag + x0) + (x2 + x1).
 template <int N, int W>
-__global__ void __launch_bounds__(32 * W, W == 1 ? WarpCfg<N>::kMinBlocksOwn : 1)
+__global__ void __launch_bounds__(32 * W, W == 1 ? WarpCfg<N>::kMinBlocksOwn : WarpCfg<N>::kMinBlocksDyn)
     euler_cart_own_kernel(int64_t E, const DMat<N> Dm, double gm1, const double* __restrict__ U,
                           double* __restrict__ R) {
   using Cfg = WarpCfg<N>;
