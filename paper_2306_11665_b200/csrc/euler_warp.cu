@@ -64,6 +64,9 @@
 #ifndef SFB_WARP_DYN_N3
 #define SFB_WARP_DYN_N3 12  // one 12-warp CTA per SM (168 regs): 0.551 -> 0.523 ms (config-4 point; 8 warps 0.532)
 #endif
+#ifndef SFB_WARP_DYN_N5
+#define SFB_WARP_DYN_N5 1  // n = 5 stays on the CTA kernel (SFB_WARP_SMALL): here W = 1/8/12 measured 0.914/0.787/0.866 vs 0.787 ms
+#endif
 #ifndef SFB_WARP_MB_N2
 #define SFB_WARP_MB_N2 1
 #endif
@@ -462,7 +465,8 @@ int launch_euler_cart_warp(int64_t E, const double* Dh, double gamma, double sca
   for (int i = 0; i < N * N; ++i) Dm.d[i] = scale * Dh[i];
   constexpr int W = (N == 4) ? SFB_WARP_DYN_N4
                    : (N == 3) ? SFB_WARP_DYN_N3
-                   : (N == 2) ? SFB_WARP_DYN_N2 : 1;  // warps per CTA (W > 1: dynamic)
+                   : (N == 2) ? SFB_WARP_DYN_N2
+                   : (N == 5) ? SFB_WARP_DYN_N5 : 1;  // warps per CTA (W > 1: dynamic)
   constexpr size_t smem = W * Cfg::kSmemOwn;
   auto kern = euler_cart_own_kernel<N, W>;
   static DeviceCache cache;
