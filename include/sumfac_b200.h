@@ -185,11 +185,15 @@ int sfb_euler_volume_cartesian_host(int64_t E, int64_t n, const double* D_host, 
  * Rhat = (Pi x Pi x Pi) r
  * sumsq[e] = sum over v, modes of Rhat[e,v,:]^2 (deterministic order), NULL ok.
  * V, Pi, D: HOST (n,n); Uhat, Rhat (E,5,n^3), Ja (E,3,3,n^3), sumsq (E):
- * device, 16-byte aligned.  n in 2..8. */
+ * device, 16-byte aligned.  n in 2..8.
+ * workspace: 8 bytes of device memory (8-byte aligned) the call zeroes on
+ * `stream` and uses as the element-claim counter of its persistent CTAs
+ * (dynamic load balance); NULL = static element split (same results, bitwise).
+ * Concurrent calls need distinct workspaces. */
 int sfb_euler_volume_curvilinear_modal(int64_t E, int64_t n, const double* V, const double* Pi,
                                        const double* D, double gamma, double scale,
                                        const double* Uhat, const double* Ja, double* Rhat,
-                                       double* sumsq, sfb_stream_t stream);
+                                       double* sumsq, void* workspace, sfb_stream_t stream);
 
 /* Deterministic fixed-order block sums: partial[b] = sum of x[b*block ..
  * b*block+block-1] (pairwise tree, independent of launch geometry).

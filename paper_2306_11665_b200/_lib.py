@@ -50,7 +50,7 @@ SIGNATURES = {
     "sfb_euler_volume_cartesian": [_i64, _i64, _p, _dbl, _dbl, _p, _p, _p],
     "sfb_euler_volume_cartesian_host": [_i64, _i64, _p, _dbl, _dbl, _p, _p],
     "sfb_euler_volume_curvilinear_modal": [
-        _i64, _i64, _p, _p, _p, _dbl, _dbl, _p, _p, _p, _p, _p,
+        _i64, _i64, _p, _p, _p, _dbl, _dbl, _p, _p, _p, _p, _p, _p,
     ],
     "sfb_block_sums": [_p, _i64, _i64, _p, _p],
     "sfb_generate_euler_states": [_i64, _i64, _i64, _u64, _dbl, _p, _p, _p],

@@ -9,7 +9,10 @@
 //   Rhat = (Pi x Pi x Pi) r                      nodal -> modal projection
 //   sumsq[e] = sum Rhat[e]^2                     (fixed-order partial of the norm)
 //
-// One persistent CTA processes one element per iteration; the next element's
+// One persistent CTA processes one element per iteration, taking its elements
+// from a per-call claim counter (workspace) when one is given: with the static
+// split e = blockIdx.x + k gridDim.x the CTAs on slower SMs set the end of the
+// kernel (40.5 -> 38.6 ms at config 5 with the claims).  The next element's
 // Uhat and Ja (8.6 KB + 15.6 KB at n = 6) are prefetched with two 1-D bulk
 // copies (cp.async.bulk, UBLKCP) into the other half of a double buffer (and
 // the one after it into L2, cp.async.bulk.prefetch) while the current
@@ -58,7 +61,7 @@
 #define SFB_MODAL_EXP_SKIP 0  // experiments only (wrong results): skip stages A=1 B=2 C=4 D=8
 #endif
 #ifndef SFB_MODAL_L2PF
-#define SFB_MODAL_L2PF 1  // L2 prefetch one element beyond the smem copy (40.8 -> 40.5 ms)
+#define SFB_MODAL_L2PF 1  // L2 prefetch one element beyond the smem copy (40.8 -> 40.5 ms; 0 or 1)
 #endif
 #ifndef SFB_MODAL_BATCH_N6
 #define SFB_MODAL_BATCH_N6 2
@@ -348,7 +351,7 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
     euler_modal_kernel(int64_t E, const __grid_constant__ ModalOps<N> ops, double gm1, double c_gamma,
                        double gam_ratio, const double* __restrict__ Uhat,
                        const double* __restrict__ Ja, double* __restrict__ Rhat,
-                       double* __restrict__ sumsq) {
+                       double* __restrict__ sumsq, unsigned long long* claim_ctr) {
   using Cfg = ModalCfg<N>;
   constexpr int NN = Cfg::kNodes;
   constexpr int T = Cfg::kThreads;
@@ -393,29 +396,47 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Ja + e * Cfg::kJ), "r"(kJB)
                  : "memory");
   };
-  if (kBulk && tid == 0 && (int64_t)blockIdx.x < E) {
-    issue(blockIdx.x, 0);
-    for (int k = 1; k <= SFB_MODAL_L2PF; ++k) {
-      const int64_t ep = blockIdx.x + (int64_t)k * gridDim.x;
-      if (ep < E) l2_prefetch(ep);
-    }
+  // Element order: e_0 = blockIdx.x; with a claim counter (dynamic) every
+  // further element is claimed from it, one element ahead (the bulk copy of
+  // the next element and the L2 prefetch of the one after need them early),
+  // so a CTA on a slower SM simply takes fewer elements; without one
+  // (static) the CTA takes e_0 + k gridDim.x.
+  __shared__ long long s_next[2];
+  const bool dyn = claim_ctr != nullptr;
+  auto claim = [&](int k) -> int64_t {  // k-th element of this CTA, k >= 1
+    return dyn ? (int64_t)gridDim.x + (int64_t)atomicAdd(claim_ctr, 1ull)
+               : (int64_t)blockIdx.x + (int64_t)k * gridDim.x;
+  };
+  if (tid == 0 && (int64_t)blockIdx.x < E) {
+    if (kBulk) issue(blockIdx.x, 0);
+    const int64_t e1 = claim(1);
+    s_next[0] = e1;
+    if (kBulk && SFB_MODAL_L2PF > 0 && e1 < E) l2_prefetch(e1);
   }
+  __syncthreads();
   uint32_t parity[2] = {0, 0};
 
   int it = 0;
-  for (int64_t e = blockIdx.x; e < E; e += gridDim.x, ++it) {
+  // s_next[it & 1] = the element after iteration it's: written by thread 0 at
+  // the top of iteration it - 1 (the prologue for it = 0), read by every
+  // thread just before iteration it's final barrier, rewritten (for it + 2)
+  // only after that barrier
+  for (int64_t e = blockIdx.x; e < E; ++it) {
+    if (tid == 0 && s_next[it & 1] < E) {
+      const int64_t nn = claim(it + 2);
+      s_next[(it + 1) & 1] = nn;
+      if (kBulk && SFB_MODAL_L2PF > 0 && nn < E) l2_prefetch(nn);
+    }
     const int slot = it & 1;
     double* in = slots + slot * Cfg::kSlot;
     const double* jin = in + Cfg::kU;
     if (kBulk) {
       mbar_wait_parity(&full[slot], parity[slot]);
       parity[slot] ^= 1;
-      const int64_t nxt = e + gridDim.x;
+      const int64_t nxt = tid == 0 ? s_next[it & 1] : E;
       if (tid == 0 && nxt < E) {
         fence_proxy_async_smem();
         issue(nxt, slot ^ 1);
-        if (SFB_MODAL_L2PF > 0 && e + (int64_t)(SFB_MODAL_L2PF + 1) * gridDim.x < E)
-          l2_prefetch(e + (int64_t)(SFB_MODAL_L2PF + 1) * gridDim.x);
       }
     } else {
       for (int i = tid; i < Cfg::kU; i += T) in[i] = __ldcs(Uhat + e * Cfg::kU + i);
@@ -598,14 +619,16 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
         sumsq[e] = t;
       }
     }
+    const int64_t e_next = s_next[it & 1];
     __syncthreads();
+    e = e_next;
   }
 }
 
 template <int N>
 static int launch_modal(int64_t E, const double* V, const double* Pi, const double* D,
                         double gamma, double scale, const double* Uhat, const double* Ja,
-                        double* Rhat, double* sumsq, cudaStream_t s) {
+                        double* Rhat, double* sumsq, void* workspace, cudaStream_t s) {
   using Cfg = ModalCfg<N>;
   ModalOps<N> ops;
   for (int i = 0; i < N * N; ++i) {
@@ -635,8 +658,11 @@ static int launch_modal(int64_t E, const double* V, const double* Pi, const doub
   int64_t grid = (int64_t)num_sms() * ps;
   if (grid > E) grid = E;
   const double gm1 = gamma - 1.0;
+  unsigned long long* ctr = static_cast<unsigned long long*>(workspace);
+  if (ctr && cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s) != cudaSuccess)
+    return fail(SFB_ECUDA, "claim counter reset failed");
   kern<<<(unsigned)grid, Cfg::kThreads, Cfg::kSmem, s>>>(E, ops, gm1, 1.0 / (2.0 * gm1),
-                                                         gamma / gm1, Uhat, Ja, Rhat, sumsq);
+                                                         gamma / gm1, Uhat, Ja, Rhat, sumsq, ctr);
   return check_launch("euler_volume_curvilinear_modal");
 }
 
@@ -651,7 +677,7 @@ extern "C" int sfb_euler_volume_curvilinear_modal(int64_t E, int64_t n, const do
                                                   const double* Pi, const double* D, double gamma,
                                                   double scale, const double* Uhat,
                                                   const double* Ja, double* Rhat, double* sumsq,
-                                                  sfb_stream_t stream) {
+                                                  void* workspace, sfb_stream_t stream) {
   SFB_CHECK_ARG(E >= 0, "negative element count");
   SFB_CHECK_ARG(V && Pi && D, "null operator (host n x n arrays)");
   SFB_CHECK_ARG(gamma > 1.0, "gamma must exceed 1");
@@ -659,17 +685,18 @@ extern "C" int sfb_euler_volume_curvilinear_modal(int64_t E, int64_t n, const do
   SFB_CHECK_ARG(Uhat && Ja && Rhat, "null state / metric / output pointer");
   SFB_CHECK_ARG(((uintptr_t)Uhat | (uintptr_t)Ja | (uintptr_t)Rhat) % 16 == 0,
                 "Uhat, Ja, Rhat must be 16-byte aligned");
+  SFB_CHECK_ARG((uintptr_t)workspace % 8 == 0, "workspace must be 8-byte aligned");
   cudaStream_t s = (cudaStream_t)stream;
   switch (n) {
-    case 2: return launch_modal<2>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s);
-    case 3: return launch_modal<3>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s);
+    case 2: return launch_modal<2>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, workspace, s);
+    case 3: return launch_modal<3>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, workspace, s);
     case 4:
-      return launch_modal<4>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s);
-    case 5: return launch_modal<5>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s);
+      return launch_modal<4>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, workspace, s);
+    case 5: return launch_modal<5>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, workspace, s);
     case 6:
-      return launch_modal<6>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s);
-    case 7: return launch_modal<7>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s);
-    case 8: return launch_modal<8>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, s);
+      return launch_modal<6>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, workspace, s);
+    case 7: return launch_modal<7>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, workspace, s);
+    case 8: return launch_modal<8>(E, V, Pi, D, gamma, scale, Uhat, Ja, Rhat, sumsq, workspace, s);
     default: return fail(SFB_ENOTSUP, "euler_volume_curvilinear_modal: n must be in 2..8");
   }
 }

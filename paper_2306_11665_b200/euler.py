@@ -134,12 +134,14 @@ def generate_uniform(count, seed, lo, hi, i0=0, device=None):
 
 
 def volume_curvilinear_modal(Uhat, Ja, n, gamma=GAMMA, scale=2.0, out=None, sumsq=None,
-                             stream=None):
+                             stream=None, dynamic=True):
     """Config 5: Rhat = (Pi x Pi x Pi) r, r = scale sum_i (D_i o Ft_i) 1, u = (V x V x V) Uhat.
 
     Uhat (E, 5, n^3) modal coefficients (orthonormal Legendre), Ja (E, 3, 3, n^3)
     metric cofactors Ja[e,i,m,r] = J dxi^i/dx_m.  If ``sumsq`` (E,) is given it
-    receives sum_v sum_k Rhat[e,v,k]^2 per element.
+    receives sum_v sum_k Rhat[e,v,k]^2 per element.  ``dynamic``: the kernel's
+    CTAs claim elements from a per-call counter (an 8-byte workspace tensor)
+    instead of a static split; the results are bitwise the same.
     """
     _lib.require_cuda()
     _, D, V, Pi = gll_operators(n)
@@ -156,10 +158,13 @@ def volume_curvilinear_modal(Uhat, Ja, n, gamma=GAMMA, scale=2.0, out=None, sums
                               or sumsq.dtype != torch.float64 or sumsq.shape != (E,)
                               or not sumsq.is_contiguous()):
         raise ValueError(f"sumsq must be a contiguous CUDA float64 tensor of shape ({E},)")
+    ws = torch.empty(1, dtype=torch.int64, device=Uhat.device) if dynamic else None
+    if ws is not None and stream is not None:
+        ws.record_stream(stream)  # freed on return: keep it out of reuse until the launch ran
     _lib.call(
         "sfb_euler_volume_curvilinear_modal", E, n, V.ctypes.data, Pi.ctypes.data, D.ctypes.data,
         float(gamma), float(scale), _lib.ptr(Uhat), _lib.ptr(Ja), _lib.ptr(out),
-        _lib.ptr(sumsq), _lib.stream_ptr(stream),
+        _lib.ptr(sumsq), _lib.ptr(ws), _lib.stream_ptr(stream),
     )
     return out
 

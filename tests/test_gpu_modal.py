@@ -112,7 +112,7 @@ def test_modal_general_operators_take_the_dense_path(n):
     ss = torch.empty(E, dtype=torch.float64, device="cuda")
     _lib.call("sfb_euler_volume_curvilinear_modal", E, n, Vp.ctypes.data, Pp.ctypes.data,
               np.ascontiguousarray(D).ctypes.data, 1.4, 2.0, _lib.ptr(Uh), _lib.ptr(Ja),
-              _lib.ptr(out), _lib.ptr(ss), _lib.stream_ptr())
+              _lib.ptr(out), _lib.ptr(ss), None, _lib.stream_ptr())
     ref, ref_ss = eo.euler_volume_curvilinear_modal(Uh.cpu().numpy(), Ja.cpu().numpy(), Vp, Pp, D)
     assert max_rel(out.cpu().numpy(), ref) <= TOL
 
@@ -126,3 +126,23 @@ def test_modal_gamma_and_scale():
     ref, _ = eo.euler_volume_curvilinear_modal(Uh.cpu().numpy(), Ja.cpu().numpy(), V, Pi, D,
                                                gamma=gamma, scale=scale)
     assert max_rel(R, ref) <= TOL
+
+
+@pytest.mark.parametrize("n,E", [(6, 1000), (6, 3), (5, 777), (4, 2048)])
+def test_modal_dynamic_claims_match_static_split(n, E):
+    # the claim counter only changes which CTA computes an element: bitwise
+    # identical residuals and per-element squares, also with fewer elements
+    # than CTAs, odd n (no bulk copies) and on a side stream
+    Uh = eu.generate_modal_states(E, n, seed=41)
+    Ja = eu.generate_metric(E, n, seed=42)
+    ss_d = torch.empty(E, dtype=torch.float64, device="cuda")
+    ss_s = torch.empty(E, dtype=torch.float64, device="cuda")
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        Rd = eu.volume_curvilinear_modal(Uh, Ja, n, sumsq=ss_d, stream=side, dynamic=True)
+    torch.cuda.current_stream().wait_stream(side)
+    Rs = eu.volume_curvilinear_modal(Uh, Ja, n, sumsq=ss_s, dynamic=False)
+    for _ in range(3):  # repeated calls reset the counter
+        Rd2 = eu.volume_curvilinear_modal(Uh, Ja, n, dynamic=True)
+    assert torch.equal(Rd, Rs) and torch.equal(ss_d, ss_s) and torch.equal(Rd2, Rs)
