@@ -29,8 +29,9 @@
 //            residuals into the record planes and the x2 residuals added into
 //            the diagonal term (SFB_MODAL_COMPACT: 69 KB, 3 CTAs per SM);
 //   stage D  three passes of Pi, the first summing the three buffers on the
-//            fly; Rhat streamed out; per-thread squares summed in a fixed
-//            order, xor-butterfly per warp, warps in order -> sumsq[e].
+//            fly, the last storing Rhat straight to HBM; per-thread squares
+//            summed in a fixed order, xor-butterfly per warp, warps in
+//            order -> sumsq[e].
 // The metric averaging 1/2 is folded into D (Ft is linear in n).
 #include "bulk.cuh"
 #include "common.cuh"
@@ -226,6 +227,34 @@ __device__ __forceinline__ void kron_pass(const double (&A)[N * N], const double
       for (int a = 0; a < N; ++a) out[o + a * stride] = y[a];
     }
   }
+}
+
+// The last pass (x2 lines) of Pi^3 with its lines written straight to HBM
+// (evict-first; at a given node offset the lanes of a warp cover consecutive
+// lines, so every store instruction is coalesced) and the squares of the
+// written values summed per thread in item order: no shared round trip and
+// no barrier between the last pass and the store.
+template <int N, int MODE>
+__device__ __forceinline__ double kron_pass_out(const double (&A)[N * N], const double* in,
+                                                double* __restrict__ gout, int tid,
+                                                int nthreads) {
+  constexpr int NN = N * N * N;
+  double ss = 0.0;
+  for (int t = tid; t < 5 * N * N; t += nthreads) {
+    const int v = t / (N * N);
+    const int L = t - v * N * N;
+    const int o = v * NN + L;  // x2 line (u0, u1): base u0 + u1 N = L, stride N^2
+    double x[N], y[N];
+#pragma unroll
+    for (int c = 0; c < N; ++c) x[c] = in[o + c * N * N];
+    apply_line<N, MODE>(A, x, y);
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+      __stcs(gout + o + a * N * N, y[a]);
+      ss = fma(y[a], y[a], ss);
+    }
+  }
+  return ss;
 }
 
 // Contravariant Chandrashekar flux for K pairs at once (normals n = Ja_a + Ja_b,
@@ -597,30 +626,29 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
     __syncthreads();
     kron_pass<N, MP, 1, 1>(sP, res, in, tid, T);
     __syncthreads();
-    kron_pass<N, MP, 1, 2>(sP, in, res, tid, T);  // Rhat in res
-    __syncthreads();
     }
     double* Rg = Rhat + e * Cfg::kU;
     double ss = 0.0;
-    for (int i = tid; i < Cfg::kU; i += T) {
-      const double x = res[i];
-      __stcs(Rg + i, x);
-      ss = fma(x, x, ss);
+    if (!(SFB_MODAL_EXP_SKIP & 8)) {
+      ss = kron_pass_out<N, MP>(sP, in, Rg, tid, T);  // last pass straight to HBM
+    } else {
+      for (int i = tid; i < Cfg::kU; i += T) __stcs(Rg + i, res[i]);
     }
+    const int64_t e_next = s_next[it & 1];
     if (sumsq) {  // fixed order: xor-butterfly in each warp, then the warps in order
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
       if ((tid & 31) == 0) wsum[tid >> 5] = ss;
-      __syncthreads();
+      __syncthreads();  // also the end of this element's shared-memory use
       if (tid == 0) {
         double t = wsum[0];
 #pragma unroll
         for (int w = 1; w < T / 32; ++w) t += wsum[w];
         sumsq[e] = t;
       }
+    } else {
+      __syncthreads();
     }
-    const int64_t e_next = s_next[it & 1];
-    __syncthreads();
     e = e_next;
   }
 }
