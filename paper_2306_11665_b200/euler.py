@@ -89,8 +89,9 @@ def volume_cartesian_host(U, n, D=None, gamma=GAMMA, scale=2.0, out=None):
         U_ptr, E = U.data_ptr(), U.shape[0]
         if out is None:
             out = torch.empty_like(U)
-        elif out.is_cuda or out.shape != U.shape or out.dtype != torch.float64:
-            raise ValueError("out must be a float64 host tensor shaped like U")
+        elif (not isinstance(out, torch.Tensor) or out.is_cuda or out.shape != U.shape
+              or out.dtype != torch.float64 or not out.is_contiguous()):
+            raise ValueError("out must be a contiguous float64 host tensor shaped like U")
         R_ptr = out.data_ptr()
     else:
         U = np.ascontiguousarray(U, dtype=np.float64)
@@ -99,6 +100,9 @@ def volume_cartesian_host(U, n, D=None, gamma=GAMMA, scale=2.0, out=None):
             raise ValueError(f"U must have shape (E, 5, {n**3})")
         if out is None:
             out = np.empty_like(U)
+        elif (not isinstance(out, np.ndarray) or out.dtype != np.float64 or out.shape != U.shape
+              or not out.flags.c_contiguous or not out.flags.writeable):
+            raise ValueError("out must be a writeable C-contiguous float64 ndarray shaped like U")
         U_ptr, R_ptr = U.ctypes.data, out.ctypes.data
     _lib.call(
         "sfb_euler_volume_cartesian_host", E, n, D.ctypes.data, float(gamma), float(scale),

@@ -65,6 +65,21 @@ def test_bad_arguments_raise():
     with pytest.raises(NotImplementedError):
         eu.volume_cartesian(torch.empty((2, 5, 729), dtype=torch.float64, device="cuda"), 9,
                             D=np.eye(9))
+    # host entry: outputs that the library would write through must be checked
+    Uh = U.cpu().numpy()
+    for bad in (np.empty((3, 5, 64), dtype=np.float32), np.empty((2, 5, 64)),
+                np.empty((3, 64, 5)).transpose(0, 2, 1), torch.empty((3, 5, 64), dtype=torch.float64)):
+        with pytest.raises(ValueError):
+            eu.volume_cartesian_host(Uh, n, out=bad)
+    ro = np.empty((3, 5, 64))
+    ro.flags.writeable = False
+    with pytest.raises(ValueError):
+        eu.volume_cartesian_host(Uh, n, out=ro)
+    Ut = U.cpu()
+    for bad in (torch.empty((3, 64, 5), dtype=torch.float64).transpose(1, 2), torch.empty_like(U),
+                np.empty((3, 5, 64))):
+        with pytest.raises(ValueError):
+            eu.volume_cartesian_host(Ut, n, out=bad)
 
 
 def test_constant_state_is_steady_full_size():
