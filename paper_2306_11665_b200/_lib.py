@@ -122,6 +122,10 @@ def ptr(t):
     if isinstance(t, torch.Tensor):
         if not t.is_contiguous():
             raise ValueError("tensor must be contiguous")
+        if t.is_cuda and t.device.index != torch.cuda.current_device():
+            # the library launches on the current device (C ABI convention)
+            raise ValueError(f"tensor on {t.device} but the current device is "
+                             f"cuda:{torch.cuda.current_device()} (use torch.cuda.device)")
         return t.data_ptr()
     # numpy array (host pointer)
     if not t.flags["C_CONTIGUOUS"]:
