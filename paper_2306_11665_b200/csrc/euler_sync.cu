@@ -17,7 +17,10 @@
 // n = 6 only (0.95 vs 1.01 ms, the default there); at n = 5, 7, 8 the
 // warp-specialised kernel stays ahead (0.79 / 1.34 / 1.27 vs 1.00 / 1.46 /
 // 1.33 ms here): the lean pair loop has little ILP and the extra warps do not
-// make up for the CTA barriers and the records stage's idle lanes.
+// make up for the CTA barriers and the records stage's idle lanes.  (ncu:
+// LDCU - the pair loop's D coefficients from the parameter bank - is 15% of
+// the stall samples, but the coefficients from shared memory measured slower,
+// 0.983 vs 0.953 ms.)
 //
 // Per element (persistent CTAs, grid = resident CTAs; the next element's
 // states stream into the other slot by one 1-D bulk copy (UBLKCP) on an
