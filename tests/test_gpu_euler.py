@@ -135,6 +135,9 @@ def test_host_buffer_entry_matches_device_entry():
     assert torch.equal(Rh, Rd.cpu())
     Rn = eu.volume_cartesian_host(U.cpu().numpy(), n)  # pageable numpy path
     assert np.array_equal(Rn, Rd.cpu().numpy())
+    out = np.full((E, 5, 64), np.nan)  # caller-supplied numpy output
+    assert eu.volume_cartesian_host(U.cpu().numpy(), n, out=out) is out
+    assert np.array_equal(out, Rd.cpu().numpy())
 
 
 @pytest.mark.parametrize("n,E", [(4, 100003), (3, 77777), (6, 30001)])
