@@ -18,6 +18,17 @@ collective; timing is the max over ranks).
   --config 5   curvilinear modal Euler, n = 6, 2^21 elements sharded over the
                ranks (strong scaling) + the deterministic NCCL residual norm
 
+Under torchrun (N > 1) the default line keeps config 3 as `value` (weak
+scaling, comparable across N) and adds "config5_sharded": the north star's
+sharded config at N ranks (2^21 elements split in whole norm blocks, NCCL
+all_gather of the block partials, norm checked bitwise against the 1-rank
+value, comm_nranks from a collective over the group).
+
+Correctness gate (the reference's bench.py:134-164 _gate_point): before any
+config is timed, sampled elements of the device result are compared with the
+C oracle at max_rel <= 1e-12 (bitwise for config 2); a failure raises
+CorrectnessGateError and the run exits non-zero without a line.
+
 Rank 0 prints ONE JSON line.  Keys beyond the driver contract:
   element_dof_per_s     nodes / s (x5 for conserved DOF / s)
   roofline              dominant kernel vs measured HBM copy bandwidth
@@ -25,6 +36,15 @@ Rank 0 prints ONE JSON line.  Keys beyond the driver contract:
   cpu_baseline          the oracle's C port on the host cores (N=1, rank 0)
   e2e                   through the C-ABI host-buffer entry point (pinned
                         host buffers; H2D + kernel + D2H inside the timed region)
+  gate                  the correctness gate's result for the timed config
+  other_configs         configs 2, 4, 5 at N=1, each with gate, cpu_baseline
+                        and e2e (config 4: CPU sum-factorized vs dense O(n^{2d})
+                        per DOF)
+
+The reference arm (--impl reference) never imports the product package: its
+inputs come from oracle/workload.py (synth.py loaded by file path, operators
+recorded from the reference itself) and it asserts that libsumfac_b200.so is
+not mapped into the process before timing.
 """
 
 import argparse
@@ -181,32 +201,100 @@ def workload_config(args, world):
 # ---------------------------------------------------------------------------
 # reference arm: the oracle's C port on the host cores (rank 0 only)
 # ---------------------------------------------------------------------------
+def assert_product_not_loaded(where):
+    from oracle import workload
+
+    libs = workload.loaded_native_libraries()
+    bad = [x for x in libs if "libsumfac_b200" in x]
+    if bad:
+        raise RuntimeError(f"{where}: the product library is mapped into this process ({bad})")
+    return libs
+
+
+def cpu_dense_vs_sumfac(threads, budget_s=1.0, ns=range(2, 9)):
+    """Config 4's CPU comparison: the C port of the sum-factorized route and of
+    the dense O(n^{2d}) route (oracle.py:54-112 with the Chandrashekar operand:
+    every entry of the n^d x n^d factor and flux matrices formed), per DOF, on
+    fixed element samples (config-4 inputs, seed 4)."""
+    from oracle import c_oracle, workload
+
+    syn = workload.synth()
+    pts = []
+    for n in ns:
+        D = workload.gll_operators(n)[1]
+        row = {"n": n}
+        # DOF per thread and call: ~50-100 ms of work, so thread start-up is noise
+        for route, fn, dof in (("sumfac", c_oracle.euler_volume_cartesian, 1 << 16),
+                               ("dense", c_oracle.euler_volume_dense, 1 << 12)):
+            sample = threads * max(1, -(-dof // n**3))
+            U = syn.euler_states(sample, n, seed=4)
+            fn(U[:threads], D, threads=threads)
+            t, reps = time.perf_counter(), 0
+            while True:
+                fn(U, D, threads=threads)
+                reps += 1
+                if time.perf_counter() - t > budget_s:
+                    break
+            sec = (time.perf_counter() - t) / reps
+            row[f"{route}_ns_per_dof"] = sec * 1e9 / (sample * n**3)
+            row[f"{route}_sample_elements"] = sample
+        pts.append(row)
+    ns_ = np.array([p["n"] for p in pts], dtype=float)
+    out = {"points": pts, "threads": threads, "cpu": cpu_model()}
+    hi = ns_ >= 5
+    for route, exp in (("sumfac", "1 (O(n^{d+1}) per element)"), ("dense", "3 (O(n^{2d}))")):
+        t = np.array([p[f"{route}_ns_per_dof"] for p in pts])
+        out[f"{route}_slope_per_dof_vs_n"] = {
+            "all_n": float(np.polyfit(np.log(ns_), np.log(t), 1)[0]), "expected": exp,
+            "n5_to_8": float(np.polyfit(np.log(ns_[hi]), np.log(t[hi]), 1)[0])
+            if hi.sum() >= 2 else None}
+    out["dense_over_sumfac"] = {p["n"]: p["dense_ns_per_dof"] / p["sumfac_ns_per_dof"]
+                                for p in pts}
+    return out
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
-    from oracle import c_oracle
-    from paper_2306_11665_b200 import synth
-    from paper_2306_11665_b200.operators import gauss_lobatto_legendre, lagrange_diff_matrix
+    from oracle import c_oracle, workload
 
+    syn = workload.synth()
     threads = os.cpu_count() or 1
+    extra = {}
+    unit = "entries/s"
+    metric = METRIC
     if args.config == 2:
         n, E = 4, args.elements
-        D = lagrange_diff_matrix(gauss_lobatto_legendre(n))
-        # B_j[R,l] = D[r_j, l] (weights ones), as assemble_basis builds it
-        r = np.arange(n**3)
-        basis = np.stack([D[(r // n**j) % n] for j in range(3)])
-        F = synth.uniform_array(E * 768, 2, -1.0, 1.0).reshape(E, 3, 64, 4)
+        basis = workload.config2_basis(n)
+        F = syn.uniform_array(E * 768, 2, -1.0, 1.0).reshape(E, 3, 64, 4)
         run = lambda: c_oracle.hadamard_rowsum_batched(basis, F, threads=threads)  # noqa: E731
         units = E * 768
         sample = f"full workload ({E} elements) per step"
+        metric = "FP64 Hadamard entries/s (generic batched)"
+    elif args.config == 5:
+        n = args.n
+        E = min(args.elements, args.cpu_sample_c5)
+        nodes, D, V, Pi = workload.gll_operators(n)
+        Uh = syn.modal_states(E, n, seed=5)
+        Ja = syn.metric_cofactors(E, n, seed=6, nodes=nodes)
+        run = lambda: c_oracle.euler_volume_curvilinear_modal(  # noqa: E731
+            Uh, Ja, V, Pi, D, threads=threads)
+        units = E * n**3
+        unit = "element-DOF/s"
+        metric = "FP64 element-DOF/s (3D curvilinear modal Euler flux differencing)"
+        sample = (f"first {E} of the {args.elements} config-5 elements per step (per-DOF rate "
+                  f"of the sample; the full job would take {args.elements / E:.0f}x longer)")
     else:
         n, E = args.n, args.elements
-        D = lagrange_diff_matrix(gauss_lobatto_legendre(n))
-        U = synth.euler_states(E, n, seed=3)
+        D = workload.gll_operators(n)[1]
+        U = syn.euler_states(E, n, seed=3)
         run = lambda: c_oracle.euler_volume_cartesian(U, D, threads=threads)  # noqa: E731
         units = E * 3 * n**4
         sample = f"full workload ({E} elements) per step"
+        if args.config == 4:
+            extra["cpu_dense_vs_sumfac"] = cpu_dense_vs_sumfac(threads)
+    libs = assert_product_not_loaded("reference arm")
     for _ in range(args.warmup):
         run()
     times = []
@@ -217,18 +305,20 @@ def run_reference(args):
     sec = sum(times) / len(times)
     value = units / sec
     line = {
-        "metric": METRIC if args.config != 2 else "FP64 Hadamard entries/s (generic batched)",
+        "metric": metric,
         "impl": "reference",
-        "value": value, "unit": "entries/s", "n_gpus": world, "steps": args.steps,
+        "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args, world),
-        "cpu_baseline": {"value": value, "unit": "entries/s", "cores": threads, "kind": "port",
+        "scaling": "strong" if args.config == 5 else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(args, world),
+        "cpu_baseline": {"value": value, "unit": unit, "cores": threads, "kind": "port",
                          "sample": f"{sample}, C port of the oracle (oracle/euler_oracle.c), "
                                    f"{threads} threads on {cpu_model()}"},
-        "e2e": {"value": value, "unit": "entries/s", "h2d_bytes_per_step": 0,
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "native_libraries_mapped": libs,
     }
+    line.update(extra)
     print(json.dumps(line), flush=True)
     return 0
 
@@ -267,6 +357,74 @@ def timed_loop(step, steps, warmup, world, dist, stream, sampler):
     return ms_total / steps, per, launches, (t0, t1)
 
 
+GATE_RTOL = 1e-12  # north star's FP64 tolerance (the reference gate: bench.py:63-64, 1e-13)
+
+
+class CorrectnessGateError(RuntimeError):
+    """A sampled element of the device result disagrees with the oracle (bench.py:134-164)."""
+
+
+def gate_sample(E, k=64, seed=0):
+    """First, last and seeded-random element ids (sorted, unique), at most k."""
+    if E <= k:
+        return np.arange(E)
+    rng = np.random.default_rng(seed)
+    idx = np.concatenate([np.arange(4), np.arange(E - 4, E), rng.choice(E, k - 8, replace=False)])
+    return np.unique(idx)
+
+
+def _gate_result(what, idx, err, tol, bitwise=None):
+    res = {"checked_elements": int(len(idx)), "max_rel": err, "tol": tol,
+           "oracle": "C port of the oracle (oracle/euler_oracle.c)", "passed": err <= tol}
+    if bitwise is not None:
+        res["bitwise"] = bitwise
+    if not res["passed"]:
+        raise CorrectnessGateError(f"{what}: max_rel {err:.3e} > {tol:.0e} on sampled elements")
+    return res
+
+
+def gate_cartesian(U, R, n, threads):
+    from oracle import c_oracle, euler_oracle, workload
+
+    import torch
+
+    idx = gate_sample(U.shape[0])
+    ti = torch.from_numpy(idx).to(U.device)
+    Us, Rs = U[ti].cpu().numpy(), R[ti].cpu().numpy()
+    ref = c_oracle.euler_volume_cartesian(Us, workload.gll_operators(n)[1], threads=threads)
+    return _gate_result(f"config 3/4 n={n}", idx, euler_oracle.max_rel(Rs, ref), GATE_RTOL)
+
+
+def gate_hadamard(F, out, n, threads):
+    from oracle import c_oracle, euler_oracle, workload
+
+    import torch
+
+    idx = gate_sample(F.shape[0])
+    ti = torch.from_numpy(idx).to(F.device)
+    ref = c_oracle.hadamard_rowsum_batched(workload.config2_basis(n), F[ti].cpu().numpy(),
+                                           threads=threads)
+    got = out[ti].cpu().numpy()
+    return _gate_result("config 2", idx, euler_oracle.max_rel(got, ref), 1e-13,
+                        bitwise=bool(np.array_equal(got, ref)))
+
+
+def gate_modal(Uh, Ja, Rh, ss, n, threads):
+    from oracle import c_oracle, euler_oracle, workload
+
+    import torch
+
+    idx = gate_sample(Uh.shape[0], k=32)
+    ti = torch.from_numpy(idx).to(Uh.device)
+    _, D, V, Pi = workload.gll_operators(n)
+    ref, ref_ss = c_oracle.euler_volume_curvilinear_modal(Uh[ti].cpu().numpy(),
+                                                          Ja[ti].cpu().numpy(), V, Pi, D,
+                                                          threads=threads)
+    err = max(euler_oracle.max_rel(Rh[ti].cpu().numpy(), ref),
+              euler_oracle.max_rel(ss[ti].cpu().numpy(), ref_ss))
+    return _gate_result("config 5", idx, err, GATE_RTOL)
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -290,12 +448,15 @@ def run_ours(args):
     sampler.start()
     time.sleep(0.3)
 
+    cpu = world == 1 and not args.no_cpu_baseline
     if args.config == 4:
-        line = run_sweep(args, world, rank, dev, stream, sampler, dist)
+        line = run_sweep(args, world, rank, dev, stream, sampler, dist, cpu=cpu)
     elif args.config == 5:
-        line = run_modal(args, world, rank, dev, stream, sampler, dist)
+        line = run_modal(args, world, rank, dev, stream, sampler, dist, cpu=cpu,
+                         e2e=world == 1 and not args.no_e2e)
     elif args.config == 2:
-        line = run_hadamard(args, world, rank, dev, stream, sampler, dist)
+        line = run_hadamard(args, world, rank, dev, stream, sampler, dist, cpu=cpu,
+                            e2e=world == 1 and not args.no_e2e)
     else:
         n, E = args.n, args.elements
         U = eu.generate_states(E, n, seed=3, e0=rank * E, device=dev)
@@ -304,6 +465,8 @@ def run_ours(args):
         def step():
             eu.volume_cartesian(U, n, out=R)
 
+        step()
+        gate = gate_cartesian(U, R, n, os.cpu_count() or 1)
         ms_step, per, launches, (t0, t1) = timed_loop(step, args.steps, args.warmup, world, dist,
                                                       stream, sampler)
         line = finish_line(args, world, dev, dist, ms_step, per, launches, sampler, t0, t1,
@@ -312,15 +475,19 @@ def run_ours(args):
                            flops_launch=euler_flops_per_element(n) * E,
                            extra={"element_dof_per_s": None, "dof_per_element": n**3},
                            traffic=ncu_traffic(args, n, E))
+        line["gate"] = gate
         line["element_dof_per_s"] = world * E * n**3 / (line["ms_per_step"] / 1e3)
         if not args.no_e2e:  # every rank its own host buffers; max over ranks
             line["e2e"] = measure_e2e(args, U, world, dist, dev)
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = measure_cpu_baseline(args, U)
+        del U, R
+        torch.cuda.empty_cache()
         if world == 1 and not args.no_extras:
-            del U, R
-            torch.cuda.empty_cache()
             line["other_configs"] = measure_other_configs(args, dev, stream, sampler, dist)
+        elif world > 1 and not args.no_extras:
+            line["config5_sharded"] = sharded_config5(args, world, rank, dev, stream, sampler,
+                                                      dist)
     sampler.stop()
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -328,6 +495,32 @@ def run_ours(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+# residual norm of the default config 5 (n = 6, 2^21 elements, seeds 5/6),
+# bitwise invariant in the rank count (shard.global_norm_tensor); measured on
+# one B200 (profiles/r01/bench_config5.json, gpurun_out/tr2c5.json)
+CONFIG5_NORM_1RANK = 0.0037271219456293993
+
+
+def sharded_config5(args, world, rank, dev, stream, sampler, dist):
+    """The north star's sharded config at this job's N ranks (strong scaling)."""
+    import copy
+
+    import torch
+
+    a = copy.copy(args)
+    a.config, a.n, a.elements, a.steps, a.warmup, a.traffic = 5, 6, 2**21, 5, 3, None
+    ln = run_modal(a, world, rank, dev, stream, sampler, dist)
+    ones = torch.ones(1, dtype=torch.float64, device=dev)
+    dist.all_reduce(ones)
+    out = {k: ln[k] for k in ("metric", "value", "unit", "ms_per_step", "scaling", "config",
+                              "roofline", "residual_norm", "per_rank_kernel_ms", "gate")}
+    out["comm_nranks"] = int(ones.item())
+    out["comm_backend"] = dist.get_backend()
+    out["norm_bitwise_equal_1rank"] = ln["residual_norm"] == CONFIG5_NORM_1RANK
+    out["norm_1rank"] = CONFIG5_NORM_1RANK
+    return out
 
 
 def ncu_traffic(args, n, elements):
@@ -389,34 +582,89 @@ def finish_line(args, world, dev, dist, ms_step, per, launches, sampler, t0, t1,
     return line
 
 
-def run_hadamard(args, world, rank, dev, stream, sampler, dist):
+def run_hadamard(args, world, rank, dev, stream, sampler, dist, cpu=False, e2e=False):
     import torch
 
     import paper_2306_11665_b200 as sf
-    from paper_2306_11665_b200 import _lib
     from paper_2306_11665_b200 import euler as eu
+    from paper_2306_11665_b200 import kernel
 
     n, d, E = 4, 3, args.elements
     D = sf.lagrange_diff_matrix(sf.gauss_lobatto_legendre(n))
     pattern = sf.build_sparsity_pattern(n, n, d)
-    basis = sf.assemble_basis_factors(pattern, D, np.ones(n)).device
-    F = eu.generate_uniform(E * 768, 2, -1.0, 1.0, i0=rank * E * 768, device=dev)
+    basis = sf.assemble_basis_factors(pattern, D, np.ones(n))
+    F = eu.generate_uniform(E * 768, 2, -1.0, 1.0, i0=rank * E * 768, device=dev).reshape(
+        E, d, 64, n)
     out = torch.empty((E, 64), dtype=torch.float64, device=dev)
+    B = basis.device
 
     def step():
-        _lib.call("sfb_hadamard_rowsum_batched", E, n, n, d, _lib.ptr(basis), _lib.ptr(F), None,
-                  _lib.ptr(out), _lib.stream_ptr())
+        kernel.hadamard_rowsum_batched(B, F, out=out)
 
+    step()
+    gate = gate_hadamard(F, out, n, os.cpu_count() or 1)
     ms_step, per, launches, (t0, t1) = timed_loop(step, args.steps, args.warmup, world, dist,
                                                   stream, sampler)
     line = finish_line(args, world, dev, dist, ms_step, per, launches, sampler, t0, t1,
                        units=E * 768, unit="entries/s", bytes_launch=8 * (768 + 64) * E,
-                       flops_launch=2 * 768 * E, metric="FP64 Hadamard entries/s (generic batched)")
+                       flops_launch=2 * 768 * E, metric="FP64 Hadamard entries/s (generic batched)",
+                       traffic=ncu_traffic(args, n, E))
+    line["gate"] = gate
+    if cpu:
+        line["cpu_baseline"] = cpu_baseline_hadamard(args, F)
+    if e2e:
+        line["e2e"] = e2e_hadamard(basis, F, out)
     del F, out
     torch.cuda.empty_cache()
     if world == 1:
         line["n_sweep"] = hadamard_n_sweep(dev, stream, sampler)
     return line
+
+
+def cpu_baseline_hadamard(args, F):
+    from oracle import c_oracle, workload
+
+    threads = os.cpu_count() or 1
+    basis = workload.config2_basis(4)
+    sample = min(F.shape[0], 65536)
+    Fs = F[:sample].cpu().numpy()
+    c_oracle.hadamard_rowsum_batched(basis, Fs[:1024], threads=threads)
+    t, reps = time.perf_counter(), 0
+    while True:
+        c_oracle.hadamard_rowsum_batched(basis, Fs, threads=threads)
+        reps += 1
+        if time.perf_counter() - t > args.cpu_seconds_extra:
+            break
+    sec = (time.perf_counter() - t) / reps
+    return {"value": sample * 768 / sec, "unit": "entries/s", "cores": threads, "kind": "port",
+            "sample": f"{sample} of the {F.shape[0]} config-2 elements x {reps} reps, C port of "
+                      f"the reference pipeline (oracle/euler_oracle.c), {threads} threads on "
+                      f"{cpu_model()}"}
+
+
+def e2e_hadamard(basis, F_dev, out_dev, steps=5):
+    """Config 2 through the host-buffer C-ABI entry (pinned F in, pinned sums out)."""
+    import torch
+
+    from paper_2306_11665_b200 import kernel
+
+    E = F_dev.shape[0]
+    Fh = torch.empty(tuple(F_dev.shape), dtype=torch.float64, pin_memory=True)
+    Fh.copy_(F_dev.cpu())
+    Oh = torch.empty((E, 64), dtype=torch.float64, pin_memory=True)
+    kernel.hadamard_rowsum_batched_host(basis, Fh, out=Oh)
+    times = []
+    for _ in range(steps):
+        t = time.perf_counter()
+        kernel.hadamard_rowsum_batched_host(basis, Fh, out=Oh)
+        times.append(time.perf_counter() - t)
+    sec = float(np.mean(times))
+    assert torch.equal(Oh, out_dev.cpu()), "config-2 e2e result differs from the device path"
+    return {"value": E * 768 / sec, "unit": "entries/s", "h2d_bytes_per_step": Fh.numel() * 8,
+            "d2h_bytes_per_step": Oh.numel() * 8, "ms_per_step": sec * 1e3, "steps": steps,
+            "path": "sfb_hadamard_rowsum_batched_host (pinned host buffers, 3-stream chunked "
+                    "H2D/kernel/D2H pipeline), wall clock per call; result bitwise equal to the "
+                    "device path"}
 
 
 def hadamard_n_sweep(dev, stream, sampler, steps=5):
@@ -457,12 +705,13 @@ def hadamard_n_sweep(dev, stream, sampler, steps=5):
             "expected_slope": "d+1 = 4 (the reference's own CPU run: 3.66, BASELINE.md)"}
 
 
-def run_sweep(args, world, rank, dev, stream, sampler, dist):
+def run_sweep(args, world, rank, dev, stream, sampler, dist, cpu=False):
     import torch
 
     from paper_2306_11665_b200 import euler as eu
 
     points = []
+    gates = {}
     t_first = None
     for n in range(2, 9):
         E = int(round(2**24 / n**3))
@@ -472,6 +721,8 @@ def run_sweep(args, world, rank, dev, stream, sampler, dist):
         def step():
             eu.volume_cartesian(U, n, out=R)
 
+        step()
+        gates[n] = gate_cartesian(U, R, n, os.cpu_count() or 1)
         ms_step, per, launches, (t0, t1) = timed_loop(step, args.steps, args.warmup, world, dist,
                                                       stream, sampler)
         t_first = t_first or t0
@@ -502,11 +753,27 @@ def run_sweep(args, world, rank, dev, stream, sampler, dist):
     line["sweep"] = points
     line["slope_time_per_dof_vs_n"] = {"all_n": slope_all, "n5_to_8": slope_cb,
                                        "expected": "1 (O(n^{d+1}) per element / n^d DOF)"}
+    line["gate"] = {"passed": all(g["passed"] for g in gates.values()),
+                    "max_rel": max(g["max_rel"] for g in gates.values()), "tol": GATE_RTOL,
+                    "per_n": {n: g["max_rel"] for n, g in gates.items()}}
+    if cpu:
+        cd = cpu_dense_vs_sumfac(os.cpu_count() or 1)
+        for p in points:
+            q = next(x for x in cd["points"] if x["n"] == p["n"])
+            p["cpu_sumfac_ns_per_dof"] = q["sumfac_ns_per_dof"]
+            p["cpu_dense_ns_per_dof"] = q["dense_ns_per_dof"]
+        line["cpu_dense_vs_sumfac"] = cd
+        p4 = next(x for x in cd["points"] if x["n"] == 4)
+        line["cpu_baseline"] = {"value": 3 * 4 / (p4["sumfac_ns_per_dof"] * 1e-9), "unit":
+                                "entries/s", "cores": cd["threads"], "kind": "port",
+                                "sample": f"{p4['sumfac_sample_elements']} config-4 elements at "
+                                          f"n=4, C port of the oracle, {cd['threads']} threads "
+                                          f"on {cd['cpu']}"}
     del best
     return line
 
 
-def run_modal(args, world, rank, dev, stream, sampler, dist):
+def run_modal(args, world, rank, dev, stream, sampler, dist, cpu=False, e2e=False):
     import torch
 
     from paper_2306_11665_b200 import euler as eu
@@ -514,18 +781,21 @@ def run_modal(args, world, rank, dev, stream, sampler, dist):
 
     n = args.n
     total = args.elements
-    e0, E = shard.shard_range(total, rank, world)
+    block = shard.job_block(total)  # one block size for the whole job
+    e0, E = shard.block_shard(total, rank, world, block)  # whole blocks per rank
     Uh = eu.generate_modal_states(E, n, seed=5, e0=e0, device=dev)
     Ja = eu.generate_metric(E, n, seed=6, e0=e0, device=dev)
     Rh = torch.empty_like(Uh)
     ss = torch.empty(E, dtype=torch.float64, device=dev)
-    block = 4096 if E % 4096 == 0 else 1
-    norm = [0.0]
+    norm = [None]
 
     def step():
         eu.volume_curvilinear_modal(Uh, Ja, n, out=Rh, sumsq=ss)
-        norm[0] = shard.global_norm(ss, block=block)
+        # device scalar: partials, NCCL all_gather, fixed tree; no host sync
+        norm[0] = shard.global_norm_tensor(ss, block=block, total=total)
 
+    step()
+    gate = gate_modal(Uh, Ja, Rh, ss, n, os.cpu_count() or 1)
     ms_step, per, launches, (t0, t1) = timed_loop(step, args.steps, args.warmup, world, dist,
                                                   stream, sampler)
     line = finish_line(args, world, dev, dist, ms_step, per, launches, sampler, t0, t1,
@@ -535,9 +805,81 @@ def run_modal(args, world, rank, dev, stream, sampler, dist):
                        metric="FP64 element-DOF/s (3D curvilinear modal Euler flux differencing)",
                        traffic=ncu_traffic(args, n, E))
     line["value"] = total * n**3 / (line["ms_per_step"] / 1e3)  # strong scaling: total DOF
-    line["residual_norm"] = norm[0]
+    line["residual_norm"] = float(norm[0].item())
     line["hadamard_entries_per_s"] = total * 3 * n**4 / (line["ms_per_step"] / 1e3)
+    line["gate"] = gate
+    step_ms = torch.tensor([float(np.mean(per))], dtype=torch.float64, device=dev)
+    if world > 1:
+        allk = [torch.empty_like(step_ms) for _ in range(world)]
+        dist.all_gather(allk, step_ms)
+        line["per_rank_kernel_ms"] = [float(x.item()) for x in allk]
+    else:
+        line["per_rank_kernel_ms"] = [float(step_ms.item())]
+    line["elements_per_rank"] = E
+    if cpu:
+        line["cpu_baseline"] = cpu_baseline_modal(args, Uh, Ja)
+    if e2e:
+        line["e2e"] = e2e_modal(args, Uh, Ja, Rh, ss)
+    del Uh, Ja, Rh, ss
+    torch.cuda.empty_cache()
     return line
+
+
+def cpu_baseline_modal(args, Uh, Ja):
+    from oracle import c_oracle, workload
+
+    n = args.n
+    threads = os.cpu_count() or 1
+    sample = min(Uh.shape[0], args.cpu_sample_c5)
+    Us, Js = Uh[:sample].cpu().numpy(), Ja[:sample].cpu().numpy()
+    _, D, V, Pi = workload.gll_operators(n)
+    c_oracle.euler_volume_curvilinear_modal(Us[:threads], Js[:threads], V, Pi, D, threads=threads)
+    t, reps = time.perf_counter(), 0
+    while True:
+        c_oracle.euler_volume_curvilinear_modal(Us, Js, V, Pi, D, threads=threads)
+        reps += 1
+        if time.perf_counter() - t > args.cpu_seconds_extra:
+            break
+    sec = (time.perf_counter() - t) / reps
+    return {"value": sample * n**3 / sec, "unit": "element-DOF/s", "cores": threads,
+            "kind": "port",
+            "sample": f"first {sample} of the {args.elements} config-5 elements x {reps} reps "
+                      f"(per-DOF rate of the sample, extrapolated: the full job would take "
+                      f"{args.elements * sec / sample:.0f} s), C port of the oracle "
+                      f"(oracle/euler_oracle.c), {threads} threads on {cpu_model()}"}
+
+
+def e2e_modal(args, Uh_dev, Ja_dev, Rh_dev, ss_dev, steps=3):
+    """Config 5 through the host-buffer C-ABI entry on an element sample (the whole
+    job's inputs are 51 GB: pinned host buffers of that size are not a sane test)."""
+    import torch
+
+    from paper_2306_11665_b200 import euler as eu
+
+    n = args.n
+    E = min(Uh_dev.shape[0], args.e2e_sample_c5)
+    Uh = eu.pinned_empty((E, 5, n**3))
+    Uh.copy_(Uh_dev[:E].cpu())
+    Ja = eu.pinned_empty((E, 3, 3, n**3))
+    Ja.copy_(Ja_dev[:E].cpu())
+    Rh = eu.pinned_empty((E, 5, n**3))
+    ss = eu.pinned_empty((E,))
+    eu.volume_curvilinear_modal_host(Uh, Ja, n, out=Rh, sumsq=ss)
+    times = []
+    for _ in range(steps):
+        t = time.perf_counter()
+        eu.volume_curvilinear_modal_host(Uh, Ja, n, out=Rh, sumsq=ss)
+        times.append(time.perf_counter() - t)
+    sec = float(np.mean(times))
+    assert torch.equal(Rh, Rh_dev[:E].cpu()) and torch.equal(ss, ss_dev[:E].cpu()), \
+        "config-5 e2e result differs from the device path"
+    return {"value": E * n**3 / sec, "unit": "element-DOF/s",
+            "h2d_bytes_per_step": (Uh.numel() + Ja.numel()) * 8,
+            "d2h_bytes_per_step": (Rh.numel() + ss.numel()) * 8, "ms_per_step": sec * 1e3,
+            "steps": steps, "sample_elements": E,
+            "path": f"sfb_euler_volume_curvilinear_modal_host on the first {E} elements "
+                    "(pinned host buffers, 3-stream chunked H2D/kernel/D2H pipeline), wall "
+                    "clock per call; result bitwise equal to the device path"}
 
 
 def measure_other_configs(args, dev, stream, sampler, dist):
@@ -547,6 +889,7 @@ def measure_other_configs(args, dev, stream, sampler, dist):
     import torch
 
     out = {}
+    keep = ("workload", "metric", "value", "unit", "ms_per_step")
     for cfg in (2, 4, 5):
         a = copy.copy(args)
         a.config = cfg
@@ -555,18 +898,27 @@ def measure_other_configs(args, dev, stream, sampler, dist):
         a.n = 6 if cfg == 5 else 4
         a.elements = 2**21 if cfg == 5 else 262144
         a.traffic = None
-        fn = {2: run_hadamard, 4: run_sweep, 5: run_modal}[cfg]
-        ln = fn(a, 1, 0, dev, stream, sampler, dist)
-        summary = {"workload": ln["config"]["workload"], "metric": ln["metric"],
-                   "value": ln["value"], "unit": ln["unit"], "ms_per_step": ln["ms_per_step"],
-                   "roofline": {k: ln["roofline"][k] for k in ("bound", "achieved", "peak", "unit",
-                                                              "frac")}}
+        with_cpu = not args.no_cpu_baseline
+        if cfg == 2:
+            ln = run_hadamard(a, 1, 0, dev, stream, sampler, dist, cpu=with_cpu,
+                              e2e=not args.no_e2e)
+        elif cfg == 4:
+            ln = run_sweep(a, 1, 0, dev, stream, sampler, dist, cpu=with_cpu)
+        else:
+            ln = run_modal(a, 1, 0, dev, stream, sampler, dist, cpu=with_cpu,
+                           e2e=not args.no_e2e)
+        summary = {k: (ln["config"]["workload"] if k == "workload" else ln[k]) for k in keep}
+        summary["roofline"] = {k: ln["roofline"][k] for k in ("bound", "achieved", "peak", "unit",
+                                                              "frac")}
+        for k in ("gate", "cpu_baseline", "e2e", "cpu_dense_vs_sumfac", "residual_norm"):
+            if k in ln:
+                summary[k] = ln[k]
         if cfg == 4:
             summary["sweep"] = [{k: p[k] for k in ("n", "elements", "ms_per_step", "ns_per_dof",
-                                                   "hbm_frac", "fp64_frac")} for p in ln["sweep"]]
+                                                   "hbm_frac", "fp64_frac", "cpu_sumfac_ns_per_dof",
+                                                   "cpu_dense_ns_per_dof") if k in p}
+                                for p in ln["sweep"]]
             summary["slope_time_per_dof_vs_n"] = ln["slope_time_per_dof_vs_n"]
-        if cfg == 5:
-            summary["residual_norm"] = ln["residual_norm"]
         if cfg == 2 and "n_sweep" in ln:
             summary["n_sweep_slope_time_per_element"] = ln["n_sweep"]["slope_time_per_element_vs_n"]
             summary["n_sweep_us_per_element"] = {p["n"]: p["us_per_element"]
@@ -675,14 +1027,13 @@ def pcie_ceiling_ms(Uh, Rh, U_dev, reps=5):
 
 
 def measure_cpu_baseline(args, U_dev):
-    from oracle import c_oracle
-    from paper_2306_11665_b200.euler import gll_operators
+    from oracle import c_oracle, workload
 
     n = args.n
     threads = os.cpu_count() or 1
     sample = min(args.elements, args.cpu_sample)
     Us = U_dev[:sample].cpu().numpy()
-    _, D, _, _ = gll_operators(n)
+    D = workload.gll_operators(n)[1]
     c_oracle.euler_volume_cartesian(Us[: max(1, sample // 10)], D, threads=threads)
     t = time.perf_counter()
     reps = 0
@@ -713,6 +1064,12 @@ def main(argv=None):
                     help="skip the configs 2/4/5 summaries appended to the default line")
     ap.add_argument("--cpu-sample", type=int, default=262144)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)  # ~10-30 s of CPU work
+    ap.add_argument("--cpu-seconds-extra", type=float, default=4.0,
+                    help="CPU work per cpu_baseline of the configs 2/5 summaries")
+    ap.add_argument("--cpu-sample-c5", type=int, default=8192,
+                    help="config-5 elements in a CPU sample (reference arm / cpu_baseline)")
+    ap.add_argument("--e2e-sample-c5", type=int, default=131072,
+                    help="config-5 elements in the host-buffer e2e leg")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch of the top kernel (default: profiles/)")
     args = ap.parse_args(argv)

@@ -161,6 +161,14 @@ int sfb_burgers_rk4(int64_t E, int64_t n, int64_t d, const double* qfactors, con
 int sfb_kronecker_apply(int64_t B, int64_t d, const int64_t* rows_1d, const int64_t* cols_1d,
                         const double* factors, const double* x, double* y, sfb_stream_t stream);
 
+/* Same, from/to HOST buffers (the config-2 end-to-end call): basis_host
+ * (d,R,n) is uploaded once, F_host (E,d,R,n) streams in and out_sum_host
+ * (E,R) streams out over element chunks, pipelined on internal streams of the
+ * current device; returns when out_sum_host is complete. */
+int sfb_hadamard_rowsum_batched_host(int64_t E, int64_t m, int64_t n, int64_t d,
+                                     const double* basis_host, const double* F_host,
+                                     double* out_sum_host);
+
 /* ---- 3-D compressible Euler, Chandrashekar flux, Cartesian (configs 3-4) ---
  * R[e,v,r] = scale * sum_j sum_l D[r_j,l] F#_j(U[e,:,r], U[e,:,r(j->l)])_v
  * with F#_j the Chandrashekar entropy-conservative two-point flux (DESIGN.md
@@ -194,6 +202,15 @@ int sfb_euler_volume_curvilinear_modal(int64_t E, int64_t n, const double* V, co
                                        const double* D, double gamma, double scale,
                                        const double* Uhat, const double* Ja, double* Rhat,
                                        double* sumsq, void* workspace, sfb_stream_t stream);
+
+/* Same, from/to HOST buffers (the config-5 end-to-end call): Uhat_host,
+ * Ja_host in, Rhat_host and (if not NULL) sumsq_host out, pipelined over
+ * element chunks on internal streams (each with its own claim counter). */
+int sfb_euler_volume_curvilinear_modal_host(int64_t E, int64_t n, const double* V,
+                                            const double* Pi, const double* D, double gamma,
+                                            double scale, const double* Uhat_host,
+                                            const double* Ja_host, double* Rhat_host,
+                                            double* sumsq_host);
 
 /* Deterministic fixed-order block sums: partial[b] = sum of x[b*block ..
  * b*block+block-1] (pairwise tree, independent of launch geometry).

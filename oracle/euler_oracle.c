@@ -48,8 +48,10 @@ typedef struct {
   double rho, v[3], p, beta, vv, lr, lb;
 } node_t;
 
-/* flux component vector for direction j (Cartesian unit normal e_j) */
-static void chandrashekar(const node_t* a, const node_t* b, int j, double gamma, double f[5]) {
+/* flux component vector for the normal nrm (e_j on Cartesian elements, the
+   averaged contravariant metric row on curvilinear ones) */
+static void chandrashekar_n(const node_t* a, const node_t* b, const double nrm[3], double gamma,
+                            double f[5]) {
   double rho_ln = logmean(a->rho, b->rho, a->lr, b->lr);
   double beta_ln = logmean(a->beta, b->beta, a->lb, b->lb);
   double vbar[3];
@@ -57,7 +59,6 @@ static void chandrashekar(const node_t* a, const node_t* b, int j, double gamma,
   double rho_bar = 0.5 * (a->rho + b->rho);
   double beta_bar = 0.5 * (a->beta + b->beta);
   double p_hat = rho_bar / (2.0 * beta_bar);
-  double nrm[3] = {j == 0 ? 1.0 : 0.0, j == 1 ? 1.0 : 0.0, j == 2 ? 1.0 : 0.0};
   double vn = vbar[0] * nrm[0] + vbar[1] * nrm[1] + vbar[2] * nrm[2];
   double f1 = rho_ln * vn;
   double fm[3];
@@ -70,6 +71,11 @@ static void chandrashekar(const node_t* a, const node_t* b, int j, double gamma,
   f[2] = fm[1];
   f[3] = fm[2];
   f[4] = f5;
+}
+
+static void chandrashekar(const node_t* a, const node_t* b, int j, double gamma, double f[5]) {
+  const double nrm[3] = {j == 0 ? 1.0 : 0.0, j == 1 ? 1.0 : 0.0, j == 2 ? 1.0 : 0.0};
+  chandrashekar_n(a, b, nrm, gamma, f);
 }
 
 /* numpy ndarray.sum(axis=-1) order over t[0..n-1] (n <= 128 here) */
@@ -89,9 +95,9 @@ static double numpy_sum(const double* t, int n) {
   return acc;
 }
 
-static void element_volume(int n, const double* D, double gamma, double scale, const double* U,
-                           double* R, node_t* nd, double* terms) {
-  const int nodes = n * n * n;
+/* primitives per node of one element's conserved U[5][nodes] (primitives(),
+   euler_oracle.py) plus the two logarithms every log mean of the node uses */
+static void node_prep(int nodes, double gamma, const double* U, node_t* nd) {
   for (int r = 0; r < nodes; ++r) {
     node_t* q = &nd[r];
     q->rho = U[r];
@@ -102,6 +108,12 @@ static void element_volume(int n, const double* D, double gamma, double scale, c
     q->lr = log(q->rho);
     q->lb = log(q->beta);
   }
+}
+
+static void element_volume(int n, const double* D, double gamma, double scale, const double* U,
+                           double* R, node_t* nd, double* terms) {
+  const int nodes = n * n * n;
+  node_prep(nodes, gamma, U, nd);
   for (int r = 0; r < nodes; ++r) {
     double total[5] = {0, 0, 0, 0, 0};
     int stride = 1;
@@ -216,5 +228,156 @@ int oracle_hadamard_rowsum_batched(int64_t E, int64_t R, int n, int d, const dou
   if (n < 1 || n > 128) return 1;
   had_ctx_t c = {R, n, d, basis, F, out_sum};
   parallel_for(E, threads, had_body, &c);
+  return 0;
+}
+
+/* ---- config 5: curvilinear modal volume term ------------------------------
+ * Rhat = (Pi x Pi x Pi) r(u), u = (V x V x V) Uhat (kron3 in euler_oracle.py:
+ * the kronecker_apply semantics of operators.py:274-318, direction 0 first),
+ * r = scale sum_i sum_l D[r_i,l] Ft_i(u_r, u_r(i->l)) with the contravariant
+ * normal (Ja[i,:](r) + Ja[i,:](r(i->l)))/2 (euler_volume_curvilinear), and the
+ * per-element sum of Rhat^2.  Sequential sums over the contracted index; the
+ * numpy oracle's einsum order may differ in the last bits (1e-13 agreement). */
+static void kron3_apply(int n, const double* A, const double* x, double* y, double* t1,
+                        double* t2) {
+  const int n2 = n * n, n3 = n2 * n;
+  for (int c = 0; c < n; ++c)
+    for (int b = 0; b < n; ++b)
+      for (int xo = 0; xo < n; ++xo) {
+        double acc = 0.0;
+        for (int a = 0; a < n; ++a) acc = acc + A[xo * n + a] * x[c * n2 + b * n + a];
+        t1[c * n2 + b * n + xo] = acc;
+      }
+  for (int c = 0; c < n; ++c)
+    for (int yo = 0; yo < n; ++yo)
+      for (int xo = 0; xo < n; ++xo) {
+        double acc = 0.0;
+        for (int b = 0; b < n; ++b) acc = acc + A[yo * n + b] * t1[c * n2 + b * n + xo];
+        t2[c * n2 + yo * n + xo] = acc;
+      }
+  for (int zo = 0; zo < n; ++zo)
+    for (int yo = 0; yo < n; ++yo)
+      for (int xo = 0; xo < n; ++xo) {
+        double acc = 0.0;
+        for (int c = 0; c < n; ++c) acc = acc + A[zo * n + c] * t2[c * n2 + yo * n + xo];
+        y[zo * n2 + yo * n + xo] = acc;
+      }
+  (void)n3;
+}
+
+typedef struct {
+  int n;
+  const double *V, *Pi, *D, *Uhat, *Ja;
+  double gamma, scale, *Rhat, *sumsq;
+} modal_ctx_t;
+
+static void modal_body(void* arg, int64_t e0, int64_t e1) {
+  modal_ctx_t* c = (modal_ctx_t*)arg;
+  const int n = c->n, nodes = n * n * n;
+  double* u = (double*)malloc(sizeof(double) * 5 * nodes);
+  double* r = (double*)malloc(sizeof(double) * 5 * nodes);
+  double* t1 = (double*)malloc(sizeof(double) * nodes);
+  double* t2 = (double*)malloc(sizeof(double) * nodes);
+  double* terms = (double*)malloc(sizeof(double) * 5 * n);
+  node_t* nd = (node_t*)malloc(sizeof(node_t) * nodes);
+  for (int64_t e = e0; e < e1; ++e) {
+    const double* Uh = c->Uhat + e * 5 * nodes;
+    const double* Ja = c->Ja + e * 9 * nodes; /* Ja[i][m][r] */
+    for (int v = 0; v < 5; ++v) kron3_apply(n, c->V, Uh + v * nodes, u + v * nodes, t1, t2);
+    node_prep(nodes, c->gamma, u, nd);
+    for (int q = 0; q < nodes; ++q) {
+      double total[5] = {0, 0, 0, 0, 0};
+      int stride = 1;
+      for (int i = 0; i < 3; ++i) {
+        int ri = (q / stride) % n;
+        for (int l = 0; l < n; ++l) {
+          int nb = q + (l - ri) * stride;
+          double nrm[3], f[5];
+          for (int m = 0; m < 3; ++m)
+            nrm[m] = 0.5 * (Ja[(i * 3 + m) * nodes + q] + Ja[(i * 3 + m) * nodes + nb]);
+          chandrashekar_n(&nd[q], &nd[nb], nrm, c->gamma, f);
+          for (int v = 0; v < 5; ++v) terms[v * n + l] = c->D[ri * n + l] * f[v];
+        }
+        for (int v = 0; v < 5; ++v) {
+          double s = numpy_sum(&terms[v * n], n);
+          total[v] = (i == 0) ? s : total[v] + s;
+        }
+        stride *= n;
+      }
+      for (int v = 0; v < 5; ++v) r[v * nodes + q] = c->scale * total[v];
+    }
+    double* Rh = c->Rhat + e * 5 * nodes;
+    double ss = 0.0;
+    for (int v = 0; v < 5; ++v) kron3_apply(n, c->Pi, r + v * nodes, Rh + v * nodes, t1, t2);
+    for (int k = 0; k < 5 * nodes; ++k) ss = ss + Rh[k] * Rh[k];
+    if (c->sumsq) c->sumsq[e] = ss;
+  }
+  free(u);
+  free(r);
+  free(t1);
+  free(t2);
+  free(terms);
+  free(nd);
+}
+
+int oracle_euler_volume_curvilinear_modal(int64_t E, int n, const double* V, const double* Pi,
+                                          const double* D, double gamma, double scale,
+                                          const double* Uhat, const double* Ja, double* Rhat,
+                                          double* sumsq, int threads) {
+  if (n < 2 || n > 16) return 1;
+  modal_ctx_t c = {n, V, Pi, D, Uhat, Ja, gamma, scale, Rhat, sumsq};
+  parallel_for(E, threads, modal_body, &c);
+  return 0;
+}
+
+/* ---- the dense O(n^{2d}) route (config 4's comparison) ---------------------
+ * What the reference's dense oracle does per element and direction j
+ * (oracle.py:54-112): the full n^d x n^d factor K_j = dense_direction_factor(
+ * D, ones, j, 3) (entry (r, c) = D[r_j, c_j] when every other digit of r and c
+ * agrees, else 0), the full two-point operand C_j[r, c] = F#_j(u_r, u_c) at
+ * every (r, c) (dense_rank_one_operand's role for a two-point flux),
+ * dense_hadamard(K_j, C_j) and the row sum over all n^d columns.  Every entry
+ * is formed, zeros included: O(n^{2d}) flux evaluations and products. */
+typedef struct {
+  int n;
+  const double *D, *U;
+  double gamma, scale, *R;
+} dense_ctx_t;
+
+static void dense_body(void* arg, int64_t e0, int64_t e1) {
+  dense_ctx_t* c = (dense_ctx_t*)arg;
+  const int n = c->n, nodes = n * n * n;
+  node_t* nd = (node_t*)malloc(sizeof(node_t) * nodes);
+  for (int64_t e = e0; e < e1; ++e) {
+    const double* U = c->U + e * 5 * nodes;
+    double* R = c->R + e * 5 * nodes;
+    node_prep(nodes, c->gamma, U, nd);
+    for (int r = 0; r < nodes; ++r) {
+      int rd[3] = {r % n, (r / n) % n, r / (n * n)};
+      double total[5] = {0, 0, 0, 0, 0};
+      for (int j = 0; j < 3; ++j) {
+        double acc[5] = {0, 0, 0, 0, 0};
+        for (int col = 0; col < nodes; ++col) {
+          int cd[3] = {col % n, (col / n) % n, col / (n * n)};
+          double k = c->D[rd[j] * n + cd[j]];
+          for (int i = 0; i < 3; ++i)
+            if (i != j) k = k * (rd[i] == cd[i] ? 1.0 : 0.0);
+          double f[5];
+          chandrashekar(&nd[r], &nd[col], j, c->gamma, f);
+          for (int v = 0; v < 5; ++v) acc[v] = acc[v] + k * f[v];
+        }
+        for (int v = 0; v < 5; ++v) total[v] = total[v] + acc[v];
+      }
+      for (int v = 0; v < 5; ++v) R[v * nodes + r] = c->scale * total[v];
+    }
+  }
+  free(nd);
+}
+
+int oracle_euler_volume_dense(int64_t E, int n, const double* D, double gamma, double scale,
+                              const double* U, double* R, int threads) {
+  if (n < 2 || n > 16) return 1;
+  dense_ctx_t c = {n, D, U, gamma, scale, R};
+  parallel_for(E, threads, dense_body, &c);
   return 0;
 }

@@ -42,6 +42,7 @@ SIGNATURES = {
     "sfb_hadamard_evaluate": [_p, _p, _i64, _p, _p],
     "sfb_hadamard_row_sum": [_p, _i64, _i64, _p, _p],
     "sfb_hadamard_rowsum_batched": [_i64, _i64, _i64, _i64, _p, _p, _p, _p, _p],
+    "sfb_hadamard_rowsum_batched_host": [_i64, _i64, _i64, _i64, _p, _p, _p],
     "sfb_burgers_volume": [_i64, _i64, _i64, _p, _p, _int, _p, _p, _p],
     "sfb_burgers_time_derivative": [_i64, _i64, _i64, _p, _p, _dbl, _dbl, _int, _p, _p, _p],
     "sfb_burgers_rk4": [_i64, _i64, _i64, _p, _p, _dbl, _dbl, _int, _dbl, _i64, _i64, _p, _p, _p,
@@ -51,6 +52,9 @@ SIGNATURES = {
     "sfb_euler_volume_cartesian_host": [_i64, _i64, _p, _dbl, _dbl, _p, _p],
     "sfb_euler_volume_curvilinear_modal": [
         _i64, _i64, _p, _p, _p, _dbl, _dbl, _p, _p, _p, _p, _p, _p,
+    ],
+    "sfb_euler_volume_curvilinear_modal_host": [
+        _i64, _i64, _p, _p, _p, _dbl, _dbl, _p, _p, _p, _p,
     ],
     "sfb_block_sums": [_p, _i64, _i64, _p, _p],
     "sfb_generate_euler_states": [_i64, _i64, _i64, _u64, _dbl, _p, _p, _p],

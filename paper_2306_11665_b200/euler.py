@@ -173,6 +173,33 @@ def volume_curvilinear_modal(Uhat, Ja, n, gamma=GAMMA, scale=2.0, out=None, sums
     return out
 
 
+def volume_curvilinear_modal_host(Uhat, Ja, n, gamma=GAMMA, scale=2.0, out=None, sumsq=None):
+    """Config 5 from/to host buffers (CPU float64 tensors, pinned for overlapped
+    copies): Uhat (E, 5, n^3) and Ja (E, 3, 3, n^3) in, Rhat (and the per-element
+    sum of squares if ``sumsq`` (E,) is given) out, through the C-ABI host entry
+    (chunked H2D / kernel / D2H pipeline)."""
+    _lib.require_cuda()
+    _, D, V, Pi = gll_operators(n)
+    for name, t, shp in (("Uhat", Uhat, (5, n**3)), ("Ja", Ja, (3, 3, n**3))):
+        if (not isinstance(t, torch.Tensor) or t.is_cuda or t.dtype != torch.float64
+                or not t.is_contiguous() or tuple(t.shape[1:]) != shp):
+            raise ValueError(f"{name} must be a contiguous float64 host tensor of shape (E, "
+                             f"{', '.join(map(str, shp))})")
+    E = Uhat.shape[0]
+    if Ja.shape[0] != E:
+        raise ValueError("Uhat and Ja element counts differ")
+    if out is None:
+        out = torch.empty_like(Uhat)
+    for name, t, shp in (("out", out, tuple(Uhat.shape)), ("sumsq", sumsq, (E,))):
+        if t is not None and (t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous()
+                              or tuple(t.shape) != shp):
+            raise ValueError(f"{name} must be a contiguous float64 host tensor of shape {shp}")
+    _lib.call("sfb_euler_volume_curvilinear_modal_host", E, n, V.ctypes.data, Pi.ctypes.data,
+              D.ctypes.data, float(gamma), float(scale), Uhat.data_ptr(), Ja.data_ptr(),
+              out.data_ptr(), None if sumsq is None else sumsq.data_ptr())
+    return out
+
+
 def generate_modal_states(E, n, seed, e0=0, device=None):
     """Device-side config-5 modal coefficients, bitwise equal to synth.modal_states."""
     _lib.require_cuda()

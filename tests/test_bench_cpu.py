@@ -6,6 +6,9 @@ import os
 import subprocess
 import sys
 
+import numpy as np
+import pytest
+
 from conftest import ROOT
 
 sys.path.insert(0, ROOT)
@@ -34,6 +37,52 @@ def test_reference_arm_line_on_cpu():
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+    # the reference arm never maps the product library (oracle/workload.py)
+    assert not any("libsumfac_b200" in x for x in line["native_libraries_mapped"])
+
+
+@pytest.mark.parametrize("config,extra", [(2, ["--elements", "2000"]),
+                                          (5, ["--cpu-sample-c5", "16"])])
+def test_reference_arm_other_configs(config, extra):
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run(
+        [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+         "--warmup", "0", "--config", str(config), *extra],
+        capture_output=True, text=True, env=env, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["value"] > 0 and line["impl"] == "reference"
+    assert line["unit"] == ("element-DOF/s" if config == 5 else "entries/s")
+    assert not any("libsumfac_b200" in x for x in line["native_libraries_mapped"])
+
+
+def test_cpu_dense_vs_sumfac_slopes():
+    cd = bench.cpu_dense_vs_sumfac(2, budget_s=0.05, ns=(4, 5, 6))
+    # dense per DOF grows ~n^3, sum-factorized ~n: the dense route loses more as n grows
+    ratios = [cd["dense_over_sumfac"][n] for n in (4, 5, 6)]
+    assert ratios == sorted(ratios) and ratios[0] > 1
+    assert cd["dense_slope_per_dof_vs_n"]["all_n"] > cd["sumfac_slope_per_dof_vs_n"]["all_n"] + 1
+
+
+def test_dense_oracle_equals_sum_factorized_oracle():
+    from oracle import c_oracle, euler_oracle, workload
+
+    syn = workload.synth()
+    for n in (2, 3, 4, 5):
+        U = syn.euler_states(3, n, seed=4)
+        D = workload.gll_operators(n)[1]
+        a = c_oracle.euler_volume_cartesian(U, D)
+        b = c_oracle.euler_volume_dense(U, D)
+        assert euler_oracle.max_rel(b, a) <= 1e-14
+
+
+def test_gate_sample_and_failure():
+    idx = bench.gate_sample(1000)
+    assert idx[0] == 0 and idx[-1] == 999 and len(idx) <= 64 and np.all(np.diff(idx) > 0)
+    assert list(bench.gate_sample(5)) == [0, 1, 2, 3, 4]
+    with pytest.raises(bench.CorrectnessGateError):
+        bench._gate_result("x", idx, 1e-9, 1e-12)
+    assert bench._gate_result("x", idx, 1e-15, 1e-12)["passed"]
 
 
 def test_reference_arm_non_zero_ranks_exit_quietly():

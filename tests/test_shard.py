@@ -68,3 +68,43 @@ def test_global_norm_is_world_size_invariant(world):
     det, red = q.get()
     assert det == ref  # bitwise: fixed block partials + fixed global tree
     assert abs(red - ref) <= 1e-14 * ref
+
+
+def test_job_block_and_block_shard():
+    assert shard.job_block(2**21) == 4096
+    assert shard.job_block(3 * 1024) == 1024
+    assert shard.job_block(7) == 1
+    for total, world in ((2**21, 3), (2**21, 6), (4096 * 5, 4), (12, 8)):
+        b = shard.job_block(total)
+        spans = [shard.block_shard(total, r, world, b) for r in range(world)]
+        assert spans[0][0] == 0 and spans[-1][0] + spans[-1][1] == total
+        for (a, ca), (c, _) in zip(spans, spans[1:]):
+            assert a + ca == c and a % b == 0 and ca % b == 0
+
+
+def _worker_uneven(rank, world, port, total, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    x = torch.from_numpy(np.random.default_rng(7).uniform(0, 1, total))
+    block = shard.job_block(total)
+    e0, cnt = shard.block_shard(total, rank, world, block)
+    local = x[e0:e0 + cnt].contiguous()
+    a = float(shard.global_norm_tensor(local, block=block, total=total))
+    b = shard.global_norm(local, block=block)  # counts exchanged instead of derived
+    if rank == 0:
+        out.put((a, b))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_global_norm_uneven_block_shards(world):
+    # 5 blocks of 1024 over 2 or 3 ranks: unequal block counts per rank
+    total = 5 * 1024
+    ref = shard.global_norm(torch.from_numpy(np.random.default_rng(7).uniform(0, 1, total)),
+                            block=shard.job_block(total))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.spawn(_worker_uneven, args=(world, _free_port(), total, q), nprocs=world, join=True)
+    a, b = q.get()
+    assert a == ref and b == ref
