@@ -169,6 +169,40 @@ int sfb_hadamard_rowsum_batched_host(int64_t E, int64_t m, int64_t n, int64_t d,
                                      const double* basis_host, const double* F_host,
                                      double* out_sum_host);
 
+/* ---- the reference's dense route (oracle.py) and general Kronecker passes --
+ * All device pointers; every entry of the dense matrices is formed (zeros
+ * included) with the reference's product order, so results are bitwise equal.
+ *
+ * dense_kronecker: out (prod rows, prod cols) = reduce(kron, reversed(factors))
+ *   (oracle.py:39-51); factor j (rows_1d[j] x cols_1d[j], row-major) packed
+ *   consecutively in `packed` (a diagonal factor passed as its dense diag).
+ * dense_direction_factor: out (m n^(d-1), n^d) zeroed, then the basis (m,n)
+ *   in slot `direction` times the ascending weight product (oracle.py:54-92).
+ * dense_rank_one: out (R, C) = row_values[i] col_values[j] (oracle.py:111-124).
+ * scatter_direction / gather_direction: direction `direction` of a compressed
+ *   factor (entries values) to / from its dense (row_space, column_space)
+ *   matrix through the pattern's (entries, d) rows/columns (oracle.py:127-160);
+ *   scatter zeroes `out` first.
+ * kronecker_pass: one direction of kronecker_apply (operators.py:274-318) for
+ *   any extents: y[b][h][r][a] = sum_c A[r][c] x[b][h][c][a] (a < lo, h < hi),
+ *   or y = A[r] x[...r...] when diag (A of length rows == cols). */
+int sfb_dense_kronecker(int64_t d, const int64_t* rows_1d, const int64_t* cols_1d,
+                        const double* packed, double* out, sfb_stream_t stream);
+int sfb_dense_direction_factor(int64_t m, int64_t n, int64_t d, int64_t direction,
+                               const double* basis, const double* weights, double* out,
+                               sfb_stream_t stream);
+int sfb_dense_rank_one(const double* row_values, int64_t R, const double* col_values, int64_t C,
+                       double* out, sfb_stream_t stream);
+int sfb_scatter_direction(const int64_t* rows, const int64_t* columns, int64_t d,
+                          int64_t direction, int64_t entries, const double* values,
+                          int64_t row_space, int64_t column_space, double* out,
+                          sfb_stream_t stream);
+int sfb_gather_direction(const int64_t* rows, const int64_t* columns, int64_t d,
+                         int64_t direction, int64_t entries, const double* dense,
+                         int64_t column_space, double* values, sfb_stream_t stream);
+int sfb_kronecker_pass(int64_t B, int64_t lo, int64_t rows, int64_t cols, int64_t hi, int diag,
+                       const double* A, const double* x, double* y, sfb_stream_t stream);
+
 /* ---- 3-D compressible Euler, Chandrashekar flux, Cartesian (configs 3-4) ---
  * R[e,v,r] = scale * sum_j sum_l D[r_j,l] F#_j(U[e,:,r], U[e,:,r(j->l)])_v
  * with F#_j the Chandrashekar entropy-conservative two-point flux (DESIGN.md

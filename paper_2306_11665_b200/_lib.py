@@ -48,6 +48,12 @@ SIGNATURES = {
     "sfb_burgers_rk4": [_i64, _i64, _i64, _p, _p, _dbl, _dbl, _int, _dbl, _i64, _i64, _p, _p, _p,
                         _p],
     "sfb_kronecker_apply": [_i64, _i64, _p, _p, _p, _p, _p, _p],
+    "sfb_dense_kronecker": [_i64, _p, _p, _p, _p, _p],
+    "sfb_dense_direction_factor": [_i64, _i64, _i64, _i64, _p, _p, _p, _p],
+    "sfb_dense_rank_one": [_p, _i64, _p, _i64, _p, _p],
+    "sfb_scatter_direction": [_p, _p, _i64, _i64, _i64, _p, _i64, _i64, _p, _p],
+    "sfb_gather_direction": [_p, _p, _i64, _i64, _i64, _p, _i64, _p, _p],
+    "sfb_kronecker_pass": [_i64, _i64, _i64, _i64, _i64, _int, _p, _p, _p, _p],
     "sfb_euler_volume_cartesian": [_i64, _i64, _p, _dbl, _dbl, _p, _p, _p],
     "sfb_euler_volume_cartesian_host": [_i64, _i64, _p, _dbl, _dbl, _p, _p],
     "sfb_euler_volume_curvilinear_modal": [

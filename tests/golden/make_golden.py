@@ -23,6 +23,10 @@ regenerate the same inputs without the reference):
   kron.npz             kronecker_apply on seeded factor sets
   euler_modal.npz      config 5: V^3 -> contravariant Chandrashekar volume term
                        -> Pi^3 through kronecker_apply + the index-trick route
+  dense.npz            the dense route (dense_kronecker, dense_direction_factor,
+                       dense_rank_one_operand, scatter, gather) and
+                       kronecker_apply beyond d = 3 / extents 16
+  python tests/golden/make_golden.py dense   regenerates one fixture only
 Only tests read these files; nothing on the GPU box reads /root/reference.
 """
 
@@ -328,18 +332,64 @@ def make_modal(sf):
     np.savez_compressed(os.path.join(HERE, "euler_modal.npz"), **out)
 
 
-def main():
+DENSE_DIR_CASES = [(1, 3, 3), (2, 3, 4), (2, 2, 3), (3, 4, 4), (3, 2, 5)]  # (d, m, n)
+KRON_GENERAL_CASES = [((3, 3, 3, 3), (3, 3, 3, 3), (2, 2, 2, 2)),  # extents, rows, kinds
+                      ((20, 17), (18, 21), (2, 2)),
+                      ((2, 2, 2, 2, 2), (2, 2, 2, 2, 2), (2, 1, 2, 1, 2)),
+                      ((5, 4, 3, 2), (2, 3, 4, 5), (2, 2, 2, 2))]
+
+
+def make_dense(sf):
+    out = {}
+    for k, (d, m, n) in enumerate(DENSE_DIR_CASES):
+        b = synth.uniform_array(m * n, 700 + k, -1.0, 1.0).reshape(m, n)
+        w = synth.uniform_array(n, 720 + k, 0.5, 1.5)
+        out[f"dir{k}_basis"], out[f"dir{k}_weights"] = b, w
+        for j in range(d):
+            out[f"dir{k}_out{j}"] = sf.dense_direction_factor(b, w, j, d)
+        # a Kronecker product mixing dense and diagonal slots
+        facs = [b if j % 2 == 0 else w for j in range(d)]
+        for j, f in enumerate(facs):
+            out[f"kr{k}_f{j}"] = f
+        out[f"kr{k}_out"] = sf.dense_kronecker(facs)
+        rv = synth.uniform_array(m * n ** (d - 1), 740 + k, -2.0, 2.0)
+        cv = synth.uniform_array(n**d, 760 + k, -2.0, 2.0)
+        out[f"r1{k}_rv"], out[f"r1{k}_cv"] = rv, cv
+        out[f"r1{k}_out"] = sf.dense_rank_one_operand(rv, cv)
+        pattern = sf.build_sparsity_pattern(m, n, d)
+        fac = sf.assemble_operand_factors(pattern, sf.TwoPointOperand(cv, row_values=rv))
+        for j in range(d):
+            out[f"sc{k}_out{j}"] = sf.scatter(fac.factor(j), pattern, j)
+    out["dir_cases"] = np.array(DENSE_DIR_CASES)
+    for k, (cols, rows, kinds) in enumerate(KRON_GENERAL_CASES):
+        facs = []
+        for j, (r, c, kind) in enumerate(zip(rows, cols, kinds)):
+            if kind == 1:
+                facs.append(synth.uniform_array(c, 800 + 10 * k + j, -1.0, 1.0))
+            else:
+                facs.append(synth.uniform_array(r * c, 800 + 10 * k + j, -1.0, 1.0).reshape(r, c))
+            out[f"kg{k}_f{j}"] = facs[-1]
+        v = synth.uniform_array(int(np.prod(cols)), 880 + k, -1.0, 1.0)
+        out[f"kg{k}_v"] = v
+        out[f"kg{k}_y"] = sf.kronecker_apply(facs, v)
+        out[f"kg{k}_d"] = np.array(len(cols))
+    out["kg_cases"] = np.array(len(KRON_GENERAL_CASES))
+    np.savez_compressed(os.path.join(HERE, "dense.npz"), **out)
+
+
+TARGETS = {
+    "operators": make_operators, "patterns": make_patterns, "config1": make_config1,
+    "config2": make_config2, "euler": make_euler, "burgers": make_burgers,
+    "burgers_rk4": make_burgers_rk4, "kron": make_kron, "modal": make_modal, "dense": make_dense,
+}
+
+
+def main(argv=None):
+    names = (sys.argv[1:] if argv is None else argv) or list(TARGETS)
     sf = import_reference()
-    make_operators(sf)
-    make_patterns(sf)
-    make_config1(sf)
-    make_config2(sf)
-    make_euler(sf)
-    make_burgers(sf)
-    make_burgers_rk4(sf)
-    make_kron(sf)
-    make_modal(sf)
-    print("golden fixtures written to", HERE)
+    for name in names:
+        TARGETS[name](sf)
+    print("golden fixtures written to", HERE, names)
 
 
 if __name__ == "__main__":

@@ -270,3 +270,19 @@ def test_modal_states_are_physical():
     J0 = synth.metric_cofactors(2, n, seed=2, amp=0.0)
     assert np.allclose(J0[:, 0, 0], h * h / 4) and np.allclose(J0[:, 0, 1], 0.0)
     assert np.all(np.isfinite(Ja))
+
+
+def test_oracle_dense_route_matches_reference_goldens():
+    """oracle/dense.py (the ref-suite shim's independent dense route) against the
+    reference's own dense outputs (tests/golden/dense.npz), bitwise."""
+    from oracle import dense as od
+
+    g = golden("dense.npz")
+    for k, (d, m, n) in enumerate(g["dir_cases"]):
+        b, w = g[f"dir{k}_basis"], g[f"dir{k}_weights"]
+        for j in range(d):
+            assert np.array_equal(od.dense_direction_factor(b, w, j, d), g[f"dir{k}_out{j}"])
+        facs = [g[f"kr{k}_f{j}"] for j in range(d)]
+        assert np.array_equal(od.dense_kronecker(facs), g[f"kr{k}_out"])
+        rv, cv = g[f"r1{k}_rv"], g[f"r1{k}_cv"]
+        assert np.array_equal(od.dense_rank_one_operand(rv, cv), g[f"r1{k}_out"])
