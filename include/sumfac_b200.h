@@ -213,6 +213,15 @@ int sfb_kronecker_pass(int64_t B, int64_t lo, int64_t rows, int64_t cols, int64_
 int sfb_euler_volume_cartesian(int64_t E, int64_t n, const double* D, double gamma, double scale,
                                const double* U, double* R, sfb_stream_t stream);
 
+/* Same with an 8-byte device workspace (8-byte aligned) the call zeroes on
+ * `stream`: the persistent kernels of n >= 5 then claim elements from it
+ * (dynamic load balance) instead of a static split; bitwise the same
+ * results.  NULL = the static split.  Concurrent calls need distinct
+ * workspaces. */
+int sfb_euler_volume_cartesian_ws(int64_t E, int64_t n, const double* D, double gamma,
+                                  double scale, const double* U, double* R, void* workspace,
+                                  sfb_stream_t stream);
+
 /* Same, from/to HOST buffers: pipelined H2D / kernel / D2H over element
  * chunks on internal streams of the current device; returns after R_host is
  * complete (also on error: nothing is left in flight on the caller's buffers).

@@ -55,6 +55,7 @@ SIGNATURES = {
     "sfb_gather_direction": [_p, _p, _i64, _i64, _i64, _p, _i64, _p, _p],
     "sfb_kronecker_pass": [_i64, _i64, _i64, _i64, _i64, _int, _p, _p, _p, _p],
     "sfb_euler_volume_cartesian": [_i64, _i64, _p, _dbl, _dbl, _p, _p, _p],
+    "sfb_euler_volume_cartesian_ws": [_i64, _i64, _p, _dbl, _dbl, _p, _p, _p, _p],
     "sfb_euler_volume_cartesian_host": [_i64, _i64, _p, _dbl, _dbl, _p, _p],
     "sfb_euler_volume_curvilinear_modal": [
         _i64, _i64, _p, _p, _p, _dbl, _dbl, _p, _p, _p, _p, _p, _p,

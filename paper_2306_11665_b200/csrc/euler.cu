@@ -505,10 +505,13 @@ int launch_euler_cart_warp(int64_t E, const double* Dh, double gamma, double sca
                            const double* U, double* R, cudaStream_t s);
 template <int N>
 int launch_euler_cart_sync(int64_t E, const double* Dh, double gamma, double scale,
-                           const double* U, double* R, cudaStream_t s);
+                           const double* U, double* R, void* ws, cudaStream_t s);
 
+// ws: optional 8-byte device claim counter (dynamic element claims of the
+// persistent CTA kernels; NULL = static split, the same results bitwise)
 int euler_cartesian_dispatch(int64_t E, int64_t n, const double* D_host, double gamma,
-                             double scale, const double* U, double* R, cudaStream_t s) {
+                             double scale, const double* U, double* R, void* ws,
+                             cudaStream_t s) {
   switch (n) {
     case 2:
       return SFB_WARP_SMALL ? launch_euler_cart_warp<2>(E, D_host, gamma, scale, U, R, s)
@@ -520,17 +523,17 @@ int euler_cartesian_dispatch(int64_t E, int64_t n, const double* D_host, double 
       if (SFB_WARP_N4) return launch_euler_cart_warp<4>(E, D_host, gamma, scale, U, R, s);
       return launch_euler_cartesian<4>(E, D_host, gamma, scale, U, R, s);
     case 5:  // warp kernel (25 of 32 lanes) measured 0.98 vs 0.84 ms: CTA kernel
-      if (SFB_SYNC_N5) return launch_euler_cart_sync<5>(E, D_host, gamma, scale, U, R, s);
+      if (SFB_SYNC_N5) return launch_euler_cart_sync<5>(E, D_host, gamma, scale, U, R, ws, s);
       return SFB_WARP_SMALL > 1 ? launch_euler_cart_warp<5>(E, D_host, gamma, scale, U, R, s)
                                 : launch_euler_cartesian<5>(E, D_host, gamma, scale, U, R, s);
     case 6:
-      if (SFB_SYNC_N6) return launch_euler_cart_sync<6>(E, D_host, gamma, scale, U, R, s);
+      if (SFB_SYNC_N6) return launch_euler_cart_sync<6>(E, D_host, gamma, scale, U, R, ws, s);
       return launch_euler_cartesian<6>(E, D_host, gamma, scale, U, R, s);
     case 7:
-      if (SFB_SYNC_N7) return launch_euler_cart_sync<7>(E, D_host, gamma, scale, U, R, s);
+      if (SFB_SYNC_N7) return launch_euler_cart_sync<7>(E, D_host, gamma, scale, U, R, ws, s);
       return launch_euler_cartesian<7>(E, D_host, gamma, scale, U, R, s);
     case 8:
-      if (SFB_SYNC_N8) return launch_euler_cart_sync<8>(E, D_host, gamma, scale, U, R, s);
+      if (SFB_SYNC_N8) return launch_euler_cart_sync<8>(E, D_host, gamma, scale, U, R, ws, s);
       return launch_euler_cartesian<8>(E, D_host, gamma, scale, U, R, s);
     default: return fail(SFB_ENOTSUP, "euler_volume_cartesian: n must be in 2..8");
   }
@@ -553,5 +556,23 @@ extern "C" int sfb_euler_volume_cartesian(int64_t E, int64_t n, const double* D,
   SFB_CHECK_ARG(U && R, "null state pointer");
   SFB_CHECK_ARG(((uintptr_t)U % 16) == 0 && ((uintptr_t)R % 16) == 0,
                 "U and R must be 16-byte aligned");
-  return euler_cartesian_dispatch(E, n, D, gamma, scale, U, R, (cudaStream_t)stream);
+  return euler_cartesian_dispatch(E, n, D, gamma, scale, U, R, nullptr, (cudaStream_t)stream);
+}
+
+// The same with an 8-byte device workspace: the n >= 5 persistent kernels
+// then claim elements from a counter the call zeroes on `stream` (a CTA on a
+// slower SM takes fewer elements) instead of the static split; results are
+// bitwise the same.  Concurrent calls need distinct workspaces.
+extern "C" int sfb_euler_volume_cartesian_ws(int64_t E, int64_t n, const double* D, double gamma,
+                                             double scale, const double* U, double* R,
+                                             void* workspace, sfb_stream_t stream) {
+  SFB_CHECK_ARG(E >= 0, "negative element count");
+  SFB_CHECK_ARG(D != nullptr, "null D");
+  SFB_CHECK_ARG(gamma > 1.0, "gamma must exceed 1");
+  SFB_CHECK_ARG((uintptr_t)workspace % 8 == 0, "workspace must be 8-byte aligned");
+  if (E == 0) return SFB_OK;
+  SFB_CHECK_ARG(U && R, "null state pointer");
+  SFB_CHECK_ARG(((uintptr_t)U % 16) == 0 && ((uintptr_t)R % 16) == 0,
+                "U and R must be 16-byte aligned");
+  return euler_cartesian_dispatch(E, n, D, gamma, scale, U, R, workspace, (cudaStream_t)stream);
 }

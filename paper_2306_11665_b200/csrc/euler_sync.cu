@@ -134,7 +134,8 @@ __device__ __forceinline__ void sync_batch(uint32_t rec, int base, int stride, i
 template <int N>
 __global__ void __launch_bounds__(SyncCfg<N>::kThreads) __maxnreg__(SyncCfg<N>::kMaxRegs)
     euler_cart_sync_kernel(int64_t E, const __grid_constant__ DMat<N> Dm, double gm1,
-                           const double* __restrict__ U, double* __restrict__ R) {
+                           const double* __restrict__ U, double* __restrict__ R,
+                           unsigned long long* claim_ctr) {
   using Cfg = SyncCfg<N>;
   constexpr int NN = Cfg::kNodes;
   constexpr int T = Cfg::kThreads;
@@ -172,10 +173,25 @@ __global__ void __launch_bounds__(SyncCfg<N>::kThreads) __maxnreg__(SyncCfg<N>::
                    "r"((uint32_t)copy_doubles(e) * 8u)
                    : "memory");
   };
+  // Element order: e_0 = blockIdx.x, then (with a claim counter) elements
+  // claimed one ahead from it - a CTA on a slower SM takes fewer - or
+  // (static) e_0 + k gridDim.x.  s_next[it & 1] = the element after
+  // iteration it's: written by thread 0 at the top of iteration it - 1 (the
+  // prologue for it = 0), read by every thread before iteration it's final
+  // barrier, rewritten only after it.
+  __shared__ long long s_next[2];
+  const bool dyn = claim_ctr != nullptr;
+  auto claim = [&](int k) -> int64_t {
+    return dyn ? (int64_t)gridDim.x + (int64_t)atomicAdd(claim_ctr, 1ull)
+               : (int64_t)blockIdx.x + (int64_t)k * gridDim.x;
+  };
   if (tid == 0 && (int64_t)blockIdx.x < E) {
     if (bulk_ok(blockIdx.x)) issue(blockIdx.x, 0);
-    for (int k = 1; k <= SFB_SYNC_L2PF; ++k) l2_prefetch(blockIdx.x + (int64_t)k * gridDim.x);
+    const int64_t e1 = claim(1);
+    s_next[0] = e1;
+    if (SFB_SYNC_L2PF > 0) l2_prefetch(e1);
   }
+  __syncthreads();
   uint32_t parity = 0;  // bit s = phase of slot s
 
   // stage-C geometry of this thread's line (fixed for the whole kernel)
@@ -191,7 +207,12 @@ __global__ void __launch_bounds__(SyncCfg<N>::kThreads) __maxnreg__(SyncCfg<N>::
   const uint32_t rec_s = smem_u32(rec);
 
   int it = 0;
-  for (int64_t e = blockIdx.x; e < E; e += gridDim.x, ++it) {
+  for (int64_t e = blockIdx.x; e < E; ++it) {
+    if (tid == 0 && s_next[it & 1] < E) {
+      const int64_t nn = claim(it + 2);
+      s_next[(it + 1) & 1] = nn;
+      if (SFB_SYNC_L2PF > 0) l2_prefetch(nn);
+    }
     const int slot = it & 1;
     double* in = slots + slot * Cfg::kSlot;
     if (bulk_ok(e)) {
@@ -202,12 +223,11 @@ __global__ void __launch_bounds__(SyncCfg<N>::kThreads) __maxnreg__(SyncCfg<N>::
       for (int i = tid; i < KU; i += T) in[i] = __ldcs(U + e * KU + i);
       __syncthreads();
     }
-    const int64_t nxt = e + gridDim.x;
-    if (tid == 0 && nxt < E) {
+    const int64_t nxt = tid == 0 ? s_next[it & 1] : E;
+    if (tid == 0 && nxt < E && bulk_ok(nxt)) {
       // the other slot was last read before the previous iteration's final barrier
       fence_proxy_async_smem();
-      if (bulk_ok(nxt)) issue(nxt, slot ^ 1);
-      l2_prefetch(e + (int64_t)(SFB_SYNC_L2PF + 1) * gridDim.x);
+      issue(nxt, slot ^ 1);
     }
 
     // ---- stage B: node records + diagonal term ------------------------------
@@ -288,13 +308,15 @@ __global__ void __launch_bounds__(SyncCfg<N>::kThreads) __maxnreg__(SyncCfg<N>::
     // ---- stage D: R = ((diag + x2) + x0) + x1 --------------------------------
     double* Rg = R + e * KU;
     for (int i = tid; i < KU; i += T) __stcs(Rg + i, (res[i] + in[i]) + rec[i]);
+    const int64_t e_next = s_next[it & 1];
     __syncthreads();  // res / rec / the slot are rewritten by the next element
+    e = e_next;
   }
 }
 
 template <int N>
 int launch_euler_cart_sync(int64_t E, const double* Dh, double gamma, double scale,
-                           const double* U, double* R, cudaStream_t s) {
+                           const double* U, double* R, void* ws, cudaStream_t s) {
   using Cfg = SyncCfg<N>;
   DMat<N> Dm;
   for (int i = 0; i < N * N; ++i) Dm.d[i] = scale * Dh[i];
@@ -302,18 +324,21 @@ int launch_euler_cart_sync(int64_t E, const double* Dh, double gamma, double sca
   const int ps = resident_ctas(euler_cart_sync_kernel<N>, Cfg::kThreads, Cfg::kSmem, cache);
   int64_t grid = (int64_t)num_sms() * ps;
   if (grid > E) grid = E;
+  unsigned long long* ctr = static_cast<unsigned long long*>(ws);
+  if (ctr && cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s) != cudaSuccess)
+    return fail(SFB_ECUDA, "claim counter reset failed");
   euler_cart_sync_kernel<N><<<(unsigned)grid, Cfg::kThreads, Cfg::kSmem, s>>>(E, Dm, gamma - 1.0,
-                                                                              U, R);
+                                                                              U, R, ctr);
   return check_launch("euler_volume_cartesian");
 }
 
 template int launch_euler_cart_sync<5>(int64_t, const double*, double, double, const double*,
-                                       double*, cudaStream_t);
+                                       double*, void*, cudaStream_t);
 template int launch_euler_cart_sync<6>(int64_t, const double*, double, double, const double*,
-                                       double*, cudaStream_t);
+                                       double*, void*, cudaStream_t);
 template int launch_euler_cart_sync<7>(int64_t, const double*, double, double, const double*,
-                                       double*, cudaStream_t);
+                                       double*, void*, cudaStream_t);
 template int launch_euler_cart_sync<8>(int64_t, const double*, double, double, const double*,
-                                       double*, cudaStream_t);
+                                       double*, void*, cudaStream_t);
 
 }  // namespace sfb

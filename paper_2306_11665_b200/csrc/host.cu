@@ -12,7 +12,8 @@
 
 namespace sfb {
 int euler_cartesian_dispatch(int64_t E, int64_t n, const double* D_host, double gamma,
-                             double scale, const double* U, double* R, cudaStream_t s);
+                             double scale, const double* U, double* R, void* ws,
+                             cudaStream_t s);
 
 namespace {
 constexpr int kStreams = 3;
@@ -159,8 +160,8 @@ extern "C" int sfb_euler_volume_cartesian_host(int64_t E, int64_t n, const doubl
   SFB_CHECK_ARG(a, "device ordinal out of range");
   const int64_t per = 5 * n * n * n;
   const HostArray arr[2] = {{U_host, nullptr, per}, {nullptr, R_host, per}};
-  return pipeline(*a, E, arr, [&](int64_t ne, double* const* dev, cudaStream_t s, void*) {
-    return euler_cartesian_dispatch(ne, n, D_host, gamma, scale, dev[0], dev[1], s);
+  return pipeline(*a, E, arr, [&](int64_t ne, double* const* dev, cudaStream_t s, void* ws) {
+    return euler_cartesian_dispatch(ne, n, D_host, gamma, scale, dev[0], dev[1], ws, s);
   });
 }
 

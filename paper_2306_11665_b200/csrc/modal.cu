@@ -64,6 +64,9 @@
 #ifndef SFB_MODAL_L2PF
 #define SFB_MODAL_L2PF 1  // L2 prefetch one element beyond the smem copy (40.8 -> 40.5 ms; 0 or 1)
 #endif
+#ifndef SFB_MODAL_SLOTS
+#define SFB_MODAL_SLOTS 1  // input slots: 1 = one slot, the next copy issued after the element (37.0 vs 38.0 ms with 2)
+#endif
 #ifndef SFB_MODAL_BATCH_N6
 #define SFB_MODAL_BATCH_N6 2
 #endif
@@ -92,7 +95,7 @@ struct ModalCfg {
   // residual (+ 2 direction buffers unless SFB_MODAL_COMPACT reuses the
   // record planes and the residual itself for them)
   static constexpr size_t kSmem =
-      (size_t)(2 * kSlot + kRec + (SFB_MODAL_COMPACT ? 1 : 3) * kU) * sizeof(double);
+      (size_t)(SFB_MODAL_SLOTS * kSlot + kRec + (SFB_MODAL_COMPACT ? 1 : 3) * kU) * sizeof(double);
   static constexpr int kMinBlocks = (N == 6) ? SFB_MODAL_MINBLOCKS_N6 : 1;
 };
 
@@ -389,7 +392,7 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
   // region doubles as the transform ping-pong buffer: V^3 runs slot -> res ->
   // slot -> res (u ends in res), Pi^3 runs res -> slot -> res -> slot.
   double* slots = smem;                    // [2][Uhat | Ja]
-  double* rec = smem + 2 * Cfg::kSlot;     // [7][NN] node records (natural layout)
+  double* rec = smem + SFB_MODAL_SLOTS * Cfg::kSlot;  // [7][NN] node records (natural layout)
   double* res = rec + Cfg::kRec;           // [5][NN] u, then the nodal residual r
   // x1-line residuals: the record planes once every line has read them
   // (compact), else a buffer of their own; x2-line residuals: added into the
@@ -456,14 +459,14 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
       s_next[(it + 1) & 1] = nn;
       if (kBulk && SFB_MODAL_L2PF > 0 && nn < E) l2_prefetch(nn);
     }
-    const int slot = it & 1;
+    const int slot = SFB_MODAL_SLOTS == 2 ? (it & 1) : 0;
     double* in = slots + slot * Cfg::kSlot;
     const double* jin = in + Cfg::kU;
     if (kBulk) {
       mbar_wait_parity(&full[slot], parity[slot]);
       parity[slot] ^= 1;
       const int64_t nxt = tid == 0 ? s_next[it & 1] : E;
-      if (tid == 0 && nxt < E) {
+      if (SFB_MODAL_SLOTS == 2 && tid == 0 && nxt < E) {
         fence_proxy_async_smem();
         issue(nxt, slot ^ 1);
       }
@@ -648,6 +651,10 @@ __global__ void __launch_bounds__(ModalCfg<N>::kThreads, ModalCfg<N>::kMinBlocks
       }
     } else {
       __syncthreads();
+    }
+    if (SFB_MODAL_SLOTS == 1 && kBulk && tid == 0 && e_next < E) {
+      fence_proxy_async_smem();  // the slot's last generic reads were before the barrier
+      issue(e_next, 0);
     }
     e = e_next;
   }

@@ -57,8 +57,13 @@ def _check_states(U, n, name="U"):
         raise ValueError(f"{name} must be contiguous")
 
 
-def volume_cartesian(U, n, D=None, gamma=GAMMA, scale=2.0, out=None, stream=None):
-    """R[e,:,r] = scale sum_j sum_l D[r_j,l] F#_j(U[e,:,r], U[e,:,r(j->l)])."""
+def volume_cartesian(U, n, D=None, gamma=GAMMA, scale=2.0, out=None, stream=None, dynamic=True):
+    """R[e,:,r] = scale sum_j sum_l D[r_j,l] F#_j(U[e,:,r], U[e,:,r(j->l)]).
+
+    ``dynamic``: for n >= 5 the persistent kernels claim elements from a
+    per-call counter (an 8-byte workspace tensor) instead of a static split;
+    the results are bitwise the same.
+    """
     _lib.require_cuda()
     D = _host_matrix(gll_operators(n)[1] if D is None else D, n)
     _check_states(U, n)
@@ -66,9 +71,12 @@ def volume_cartesian(U, n, D=None, gamma=GAMMA, scale=2.0, out=None, stream=None
         out = torch.empty_like(U)
     else:
         _check_states(out, n, "out")
+    ws = torch.empty(1, dtype=torch.int64, device=U.device) if dynamic and n >= 5 else None
+    if ws is not None and stream is not None:
+        ws.record_stream(stream)  # freed on return: keep it out of reuse until the launch ran
     _lib.call(
-        "sfb_euler_volume_cartesian", U.shape[0], n, D.ctypes.data, float(gamma), float(scale),
-        _lib.ptr(U), _lib.ptr(out), _lib.stream_ptr(stream),
+        "sfb_euler_volume_cartesian_ws", U.shape[0], n, D.ctypes.data, float(gamma),
+        float(scale), _lib.ptr(U), _lib.ptr(out), _lib.ptr(ws), _lib.stream_ptr(stream),
     )
     return out
 
