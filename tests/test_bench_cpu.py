@@ -57,11 +57,11 @@ def test_reference_arm_other_configs(config, extra):
 
 
 def test_cpu_dense_vs_sumfac_slopes():
-    cd = bench.cpu_dense_vs_sumfac(2, budget_s=0.05, ns=(4, 5, 6))
-    # dense per DOF grows ~n^3, sum-factorized ~n: the dense route loses more as n grows
-    ratios = [cd["dense_over_sumfac"][n] for n in (4, 5, 6)]
-    assert ratios == sorted(ratios) and ratios[0] > 1
-    assert cd["dense_slope_per_dof_vs_n"]["all_n"] > cd["sumfac_slope_per_dof_vs_n"]["all_n"] + 1
+    cd = bench.cpu_dense_vs_sumfac(2, budget_s=0.05, ns=(3, 7))
+    # dense per DOF grows ~n^3, sum-factorized ~n: between n = 3 and 7 the dense
+    # route's disadvantage grows ~(7/3)^2 ~ 5x (2x leaves room for timing noise)
+    r = cd["dense_over_sumfac"]
+    assert r[7] > 2.0 * r[3] and r[3] > 1.0
 
 
 def test_dense_oracle_equals_sum_factorized_oracle():
