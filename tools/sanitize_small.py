@@ -32,5 +32,18 @@ sf.volume_residual(sf.BurgersState(3, 4, np.linspace(-1, 1, 64)))
 sf.kronecker_apply([np.eye(3), np.ones((2, 3)), np.ones(3)], np.ones(27))
 shard.global_norm(torch.rand(4096 * 2, dtype=torch.float64, device="cuda"), block=4096)
 eu.volume_cartesian_host(eu.generate_states(5, 4, seed=4).cpu().numpy(), 4)
+# round-2 entry points: dynamic claims, dense route, general Kronecker passes, host entries
+for n in (5, 6, 7, 8):
+    eu.volume_cartesian(eu.generate_states(11, n, seed=5), n, dynamic=True)
+sf.dense_kronecker([np.ones((2, 3)), np.arange(3.0), np.eye(2)])
+sf.dense_direction_factor(np.ones((2, 3)), np.ones(3), 1, 3)
+sf.dense_rank_one_operand(np.ones(5), np.ones(7))
+sf.scatter(o, p, 2)
+sf.gather(sf.scatter(o, p, 1), p, 1)
+sf.kronecker_apply([np.ones((3, 5)), np.ones(5), np.ones((2, 5)), np.ones((4, 5))], np.ones(625))
+sf.kernel.hadamard_rowsum_batched_host(basis, F.cpu().numpy())
+Uh = eu.generate_modal_states(7, 6, seed=2).cpu()
+Ja = eu.generate_metric(7, 6, seed=3).cpu()
+eu.volume_curvilinear_modal_host(Uh, Ja, 6, sumsq=torch.empty(7, dtype=torch.float64))
 torch.cuda.synchronize()
 print("sanitize run ok")
