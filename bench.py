@@ -304,6 +304,7 @@ def run_reference(args):
         times.append(time.perf_counter() - t)
     sec = sum(times) / len(times)
     value = units / sec
+    libs = assert_product_not_loaded("reference arm (after timing)")
     line = {
         "metric": metric,
         "impl": "reference",
