@@ -109,6 +109,22 @@
 // the warp-specialised one below; config-4 points (ms, sync vs this file's):
 // n = 5 1.00 vs 0.79, n = 6 0.95 vs 1.01, n = 7 1.46 (3 CTAs at 136 regs) /
 // 1.98 (2 CTAs) vs 1.34, n = 8 1.33 vs 1.27: only n = 6 takes it
+// n = 5..8 on the lane-per-node kernel (euler_node.cu); config-4 points (ms,
+// dynamic claims; node kernel vs the default of each n): n = 5 1.00 vs 0.78,
+// n = 6 1.17 vs 0.95, n = 7 1.27 vs 1.31, n = 8 1.52 vs 1.26 - only n = 7
+// takes it
+#ifndef SFB_NODE_N5
+#define SFB_NODE_N5 0
+#endif
+#ifndef SFB_NODE_N6
+#define SFB_NODE_N6 0
+#endif
+#ifndef SFB_NODE_N7
+#define SFB_NODE_N7 1
+#endif
+#ifndef SFB_NODE_N8
+#define SFB_NODE_N8 0
+#endif
 #ifndef SFB_SYNC_N5
 #define SFB_SYNC_N5 0
 #endif
@@ -507,6 +523,10 @@ template <int N>
 int launch_euler_cart_sync(int64_t E, const double* Dh, double gamma, double scale,
                            const double* U, double* R, void* ws, cudaStream_t s);
 
+template <int N>
+int launch_euler_cart_node(int64_t E, const double* Dh, double gamma, double scale,
+                           const double* U, double* R, void* ws, cudaStream_t s);
+
 // ws: optional 8-byte device claim counter (dynamic element claims of the
 // persistent CTA kernels; NULL = static split, the same results bitwise)
 int euler_cartesian_dispatch(int64_t E, int64_t n, const double* D_host, double gamma,
@@ -523,16 +543,20 @@ int euler_cartesian_dispatch(int64_t E, int64_t n, const double* D_host, double 
       if (SFB_WARP_N4) return launch_euler_cart_warp<4>(E, D_host, gamma, scale, U, R, s);
       return launch_euler_cartesian<4>(E, D_host, gamma, scale, U, R, s);
     case 5:  // warp kernel (25 of 32 lanes) measured 0.98 vs 0.84 ms: CTA kernel
+      if (SFB_NODE_N5) return launch_euler_cart_node<5>(E, D_host, gamma, scale, U, R, ws, s);
       if (SFB_SYNC_N5) return launch_euler_cart_sync<5>(E, D_host, gamma, scale, U, R, ws, s);
       return SFB_WARP_SMALL > 1 ? launch_euler_cart_warp<5>(E, D_host, gamma, scale, U, R, s)
                                 : launch_euler_cartesian<5>(E, D_host, gamma, scale, U, R, s);
     case 6:
+      if (SFB_NODE_N6) return launch_euler_cart_node<6>(E, D_host, gamma, scale, U, R, ws, s);
       if (SFB_SYNC_N6) return launch_euler_cart_sync<6>(E, D_host, gamma, scale, U, R, ws, s);
       return launch_euler_cartesian<6>(E, D_host, gamma, scale, U, R, s);
     case 7:
+      if (SFB_NODE_N7) return launch_euler_cart_node<7>(E, D_host, gamma, scale, U, R, ws, s);
       if (SFB_SYNC_N7) return launch_euler_cart_sync<7>(E, D_host, gamma, scale, U, R, ws, s);
       return launch_euler_cartesian<7>(E, D_host, gamma, scale, U, R, s);
     case 8:
+      if (SFB_NODE_N8) return launch_euler_cart_node<8>(E, D_host, gamma, scale, U, R, ws, s);
       if (SFB_SYNC_N8) return launch_euler_cart_sync<8>(E, D_host, gamma, scale, U, R, ws, s);
       return launch_euler_cartesian<8>(E, D_host, gamma, scale, U, R, s);
     default: return fail(SFB_ENOTSUP, "euler_volume_cartesian: n must be in 2..8");
