@@ -67,6 +67,9 @@
 #ifndef SFB_MODAL_SLOTS
 #define SFB_MODAL_SLOTS 1  // input slots: 1 = one slot, the next copy issued after the element (37.0 vs 38.0 ms with 2)
 #endif
+#ifndef SFB_MODAL_PAIRITEMS
+#define SFB_MODAL_PAIRITEMS 0  // two transform items per thread side by side: 37.0 vs 36.6 ms (spills 72 -> 144 B)
+#endif
 #ifndef SFB_MODAL_BATCH_N6
 #define SFB_MODAL_BATCH_N6 2
 #endif
@@ -175,12 +178,13 @@ __device__ __forceinline__ void kron_pass(const double (&A)[N * N], const double
                                           const double* in2 = nullptr,
                                           const double* in3 = nullptr) {
   constexpr int NN = N * N * N;
+  constexpr int NI = 5 * N * N;  // (variable, line) items
   constexpr int stride = J == 0 ? 1 : (J == 1 ? N : N * N);
   // x0 lines are contiguous: 16-byte accesses (a stride-n line per lane with
   // 8-byte accesses is an n-way bank conflict pattern; 48-byte strided 16-byte
   // accesses at n = 6 cover the 32 banks once per quarter warp)
   constexpr bool kVec = (J == 0) && (N % 2 == 0);
-  for (int t = tid; t < 5 * N * N; t += nthreads) {
+  auto offset = [&](int t) {
     const int v = t / (N * N);
     const int L = t - v * N * N;
     const int u0 = L % N, u1 = L / N;
@@ -188,8 +192,9 @@ __device__ __forceinline__ void kron_pass(const double (&A)[N * N], const double
     if constexpr (J == 0) base = u0 * N + u1 * N * N;
     else if constexpr (J == 1) base = u0 + u1 * N * N;
     else base = u0 + u1 * N;
-    const int o = v * NN + base;
-    double x[N], y[N];
+    return v * NN + base;
+  };
+  auto load = [&](int o, double (&x)[N]) {
     if constexpr (kVec) {
 #pragma unroll
       for (int c = 0; c < N; c += 2) {
@@ -220,7 +225,8 @@ __device__ __forceinline__ void kron_pass(const double (&A)[N * N], const double
         }
       }
     }
-    apply_line<N, MODE>(A, x, y);
+  };
+  auto store = [&](int o, const double (&y)[N]) {
     if constexpr (kVec) {
 #pragma unroll
       for (int a = 0; a < N; a += 2)
@@ -228,6 +234,31 @@ __device__ __forceinline__ void kron_pass(const double (&A)[N * N], const double
     } else {
 #pragma unroll
       for (int a = 0; a < N; ++a) out[o + a * stride] = y[a];
+    }
+  };
+  if (SFB_MODAL_PAIRITEMS) {
+    // items t and t + nthreads side by side (two independent lines per thread:
+    // ILP for the threads that have two; each line is read completely before
+    // any line is written, and lines are disjoint, so out may alias an input)
+    for (int t = tid; t < NI; t += 2 * nthreads) {
+      const int t1 = t + nthreads;
+      const bool two = t1 < NI;
+      const int o0 = offset(t), o1 = offset(two ? t1 : t);
+      double x0[N], x1[N], y0[N], y1[N];
+      load(o0, x0);
+      load(o1, x1);
+      apply_line<N, MODE>(A, x0, y0);
+      apply_line<N, MODE>(A, x1, y1);
+      store(o0, y0);
+      if (two) store(o1, y1);
+    }
+  } else {
+    for (int t = tid; t < NI; t += nthreads) {
+      const int o = offset(t);
+      double x[N], y[N];
+      load(o, x);
+      apply_line<N, MODE>(A, x, y);
+      store(o, y);
     }
   }
 }
