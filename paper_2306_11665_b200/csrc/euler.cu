@@ -109,6 +109,14 @@
 // the warp-specialised one below; config-4 points (ms, sync vs this file's):
 // n = 5 1.00 vs 0.79, n = 6 0.95 vs 1.01, n = 7 1.46 (3 CTAs at 136 regs) /
 // 1.98 (2 CTAs) vs 1.34, n = 8 1.33 vs 1.27: only n = 6 takes it
+// n = 2 on the register-only two-threads-per-element kernel (euler_n2.cu)
+#ifndef SFB_N2_REGS
+#define SFB_N2_REGS 1
+#endif
+// n = 3 on the register/shuffle kernel, nine threads per element (euler_n3.cu)
+#ifndef SFB_N3_REGS
+#define SFB_N3_REGS 1
+#endif
 // n = 5..8 on the lane-per-node kernel (euler_node.cu); config-4 points (ms,
 // dynamic claims; node kernel vs the default of each n): n = 5 1.00 vs 0.78,
 // n = 6 1.17 vs 0.95, n = 7 1.27 vs 1.31, n = 8 1.52 vs 1.26 - only n = 7
@@ -523,6 +531,10 @@ template <int N>
 int launch_euler_cart_sync(int64_t E, const double* Dh, double gamma, double scale,
                            const double* U, double* R, void* ws, cudaStream_t s);
 
+int launch_euler_cart_n2(int64_t E, const double* Dh, double gamma, double scale,
+                         const double* U, double* R, cudaStream_t s);
+int launch_euler_cart_n3(int64_t E, const double* Dh, double gamma, double scale,
+                         const double* U, double* R, cudaStream_t s);
 template <int N>
 int launch_euler_cart_node(int64_t E, const double* Dh, double gamma, double scale,
                            const double* U, double* R, void* ws, cudaStream_t s);
@@ -534,9 +546,11 @@ int euler_cartesian_dispatch(int64_t E, int64_t n, const double* D_host, double 
                              cudaStream_t s) {
   switch (n) {
     case 2:
+      if (SFB_N2_REGS) return launch_euler_cart_n2(E, D_host, gamma, scale, U, R, s);
       return SFB_WARP_SMALL ? launch_euler_cart_warp<2>(E, D_host, gamma, scale, U, R, s)
                             : launch_euler_cartesian<2>(E, D_host, gamma, scale, U, R, s);
     case 3:  // own-line warp kernel 0.552 vs CTA kernel 0.663 ms (config 4)
+      if (SFB_N3_REGS) return launch_euler_cart_n3(E, D_host, gamma, scale, U, R, s);
       return SFB_WARP_SMALL ? launch_euler_cart_warp<3>(E, D_host, gamma, scale, U, R, s)
                             : launch_euler_cartesian<3>(E, D_host, gamma, scale, U, R, s);
     case 4:
