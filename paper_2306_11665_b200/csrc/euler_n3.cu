@@ -17,6 +17,9 @@
 // latency bound, profiles/r02/ncu_c4_n3.txt).
 #include "euler_common.cuh"
 
+#ifndef SFB_N3_L2PF
+#define SFB_N3_L2PF 1  // 0.426 vs 0.430 ms
+#endif
 #ifndef SFB_N3_THREADS
 #define SFB_N3_THREADS 128
 #endif
@@ -113,6 +116,21 @@ __global__ void __launch_bounds__(SFB_N3_THREADS, SFB_N3_MINB)
     const bool valid = lane < 27 && e_raw < E;
     const int64_t e = valid ? e_raw : 3 * g3;
     const double* u = U + e * KU + x0 + 3 * x1;
+#if SFB_N3_L2PF
+    {  // the warp's next three elements (3.2 KB contiguous) into L2
+      const int64_t ng = g3 + warps_total;
+      if (lane == 0 && 3 * ng < E) {
+        const int64_t ne = (E - 3 * ng) < 3 ? (E - 3 * ng) : 3;
+        // 16-byte granules inside [first, last) of the three elements
+        const uintptr_t a0 = (uintptr_t)(U + 3 * ng * KU) & ~(uintptr_t)15;
+        const uintptr_t a1 = (uintptr_t)(U + (3 * ng + ne) * KU) & ~(uintptr_t)15;
+        if (a1 > a0)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0),
+                       "r"((uint32_t)(a1 - a0))
+                       : "memory");
+      }
+    }
+#endif
     NodeRec rq[3];
     double acc[3][5];
 #pragma unroll
