@@ -97,3 +97,34 @@ def test_build_module_loads_without_the_library():
     assert mod.LIB_NAME == "libsumfac_b200.so"
     assert all(src.endswith(".cu") for src in mod._sources())
     assert "arch=compute_100a,code=sm_100a" in " ".join(mod.ARCH)
+
+
+def test_round2_entries_validate_without_gpu():
+    from paper_2306_11665_b200 import _lib
+
+    i64 = (ctypes.c_int64 * 2)(3, 3)
+    bad = [
+        ("sfb_dense_kronecker", (0, i64, i64, None, None, None)),             # d = 0
+        ("sfb_dense_kronecker", (17, i64, i64, None, None, None)),            # d > 16
+        ("sfb_dense_direction_factor", (2, 2, 2, 2, None, None, None, None)),  # direction >= d
+        ("sfb_dense_rank_one", (None, -1, None, 3, None, None)),             # negative extent
+        ("sfb_scatter_direction", (None, None, 2, -1, 4, None, 4, 4, None, None)),
+        ("sfb_gather_direction", (None, None, 2, 2, 4, None, 4, None, None)),
+        ("sfb_kronecker_pass", (1, 0, 3, 3, 1, 0, None, None, None, None)),  # lo = 0
+        ("sfb_kronecker_pass", (1, 1, 3, 4, 1, 1, None, None, None, None)),  # diag not square
+        ("sfb_hadamard_rowsum_batched_host", (4, 0, 4, 3, None, None, None)),
+        ("sfb_euler_volume_cartesian_host", (4, 9, None, 1.4, 2.0, None, None)),  # n > 8
+        ("sfb_euler_volume_curvilinear_modal_host", (4, 1, None, None, None, 1.4, 2.0, None,
+                                                     None, None, None)),
+    ]
+    for name, args in bad:
+        with pytest.raises(ValueError):
+            _lib.call(name, *args)
+    d = (ctypes.c_double * 4)(1, 2, 3, 4)
+    with pytest.raises(ValueError):  # workspace must be 8-byte aligned
+        _lib.call("sfb_euler_volume_cartesian_ws", 5, 6, ctypes.addressof(d), 1.4, 2.0, None,
+                  None, 3, None)
+    # nothing empty launches anything
+    _lib.call("sfb_euler_volume_cartesian_ws", 0, 6, ctypes.addressof(d), 1.4, 2.0, None, None,
+              None, None)
+    assert _lib.launch_count() == 0
