@@ -197,11 +197,12 @@ def test_many_blocks_per_cta_odd_sizes(n):
     assert max_rel(R[idx].cpu().numpy(), ref) <= TOL
 
 
-def test_log_mean_branch_band_matches_oracle():
+@pytest.mark.parametrize("n", range(2, 9))
+def test_log_mean_branch_band_matches_oracle(n):
     # element-wise perturbations of a constant state with amplitudes 1e-1..1e-7:
     # neighbour ratios sweep u = (d/s)^2 through both log-mean branches and
-    # across the ~1e-5 threshold
-    n, E = 4, 512
+    # across the ~1e-5 threshold (every n: each has its own kernel)
+    E = 512
     U = eu.generate_states(E, n, seed=21)
     base = U[:, :, :1].clone()
     amp = torch.logspace(-1, -7, E, dtype=torch.float64, device="cuda")[:, None, None]
@@ -210,12 +211,14 @@ def test_log_mean_branch_band_matches_oracle():
     _, D, _, _ = eu.gll_operators(n)
     ref = c_oracle.euler_volume_cartesian(U.cpu().numpy(), D, threads=8)
     assert max_rel(R, ref) <= TOL
-    # per element against the flux scale (the residual itself shrinks with amp)
-    scale = np.abs(U.cpu().numpy()).max(axis=(1, 2)) ** 2
-    assert (np.abs(R - ref).max(axis=(1, 2)) <= 1e-13 * scale).all()
+    # per element against the D-weighted flux scale (the residual itself shrinks
+    # with amp; rounding enters through 3(n-1) D-weighted fluxes per row, so the
+    # bound carries ||D||_inf: 2e-14 x 9.1 at n = 4, x 51 at n = 8)
+    scale = np.abs(U.cpu().numpy()).max(axis=(1, 2)) ** 2 * np.abs(D).sum(axis=1).max()
+    assert (np.abs(R - ref).max(axis=(1, 2)) <= 2e-14 * scale).all()
 
 
-@pytest.mark.parametrize("n", [2, 4, 6])
+@pytest.mark.parametrize("n", range(2, 9))
 def test_non_physical_state_is_contained(n):
     # a negative density (non-physical) makes that element's logarithms NaN;
     # the kernels are branch-free, so the NaN stays in that element and the
@@ -259,7 +262,7 @@ def test_beyond_int32_double_offsets():
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("n", [3, 4, 6])
+@pytest.mark.parametrize("n", range(2, 9))
 def test_runs_are_bitwise_reproducible(n):
     # fixed summation orders everywhere (no atomics): repeated launches agree bitwise
     U = eu.generate_states(20_000 if n < 6 else 4_000, n, seed=5)
@@ -268,7 +271,7 @@ def test_runs_are_bitwise_reproducible(n):
     assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("n", [2, 3, 4, 5, 6, 8])
+@pytest.mark.parametrize("n", range(2, 9))
 def test_general_operator_gamma_and_scale(n):
     # D, gamma and scale are parameters of the ABI: a dense random operator
     # (no GLL structure, nonzero diagonal), gamma = 5/3 and scale = -0.75
