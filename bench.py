@@ -62,14 +62,20 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 HBM_FALLBACK_GBS = 6650.0
-DFMA_MEASURED_TFLOPS = 34.154  # tools/peaks/fp64_peak.cu on this pool's B200 (profiles/)
+DFMA_MEASURED_TFLOPS = 34.214  # tools/peaks/run_fp64_peak.sh, round 2, 1965 MHz (profiles/r02/)
 METRIC = "FP64 Hadamard entries/s (3D Euler Chandrashekar flux differencing)"
 
-# Algorithmic work per element:
-# unique off-diagonal pairs x (43 flux + 20 accumulate) + diagonal entries x 18
-# + nodes x 16 (Cartesian); bytes = 2 x 5 x n^3 x 8.
-FLUX_FLOPS, ACC_FLOPS, DIAG_FLOPS, NODE_FLOPS = 43, 20, 18, 16
-CURV_EXTRA_FLOPS = 9  # contravariant: metric average (3 add) + v.n (3) + p n (3)
+# Algorithmic work per element: unique off-diagonal pairs
+# x (C_pair flux + 20 accumulate) + diagonal entries x 18 + nodes x 16; bytes =
+# 2 x 5 x n^3 x 8.  C_pair = 53 is the restated flux as written
+# (oracle/euler_oracle.py chandrashekar + logmean) in SURVEY 8(d)'s convention
+# (+, -, x, / = 1 flop), with the logarithms per node (2 per node, in NODE):
+# two log means 2 x 6, vbar 6, rhobar 2, betabar 2, p_hat 2, v.n 5, F1 1,
+# F_{1+m} 9, |v|^2 average 2, F5 12.  Cross-check, SASS of the config-3 kernel
+# (ncu, FMA = 2 flops): ~56 flops per flux.  (Round 1 used 43, the kernel's own
+# FP64 instruction count per flux with an FMA counted once.)
+FLUX_FLOPS, ACC_FLOPS, DIAG_FLOPS, NODE_FLOPS = 53, 20, 18, 16
+CURV_EXTRA_FLOPS = 6  # contravariant: the metric average n = (Ja_a + Ja_b) / 2, 3 x (add + mul)
 
 
 def euler_flops_per_element(n):
@@ -570,7 +576,7 @@ def finish_line(args, world, dev, dist, ms_step, per, launches, sampler, t0, t1,
         "roofline_fp64": {"achieved": achieved_tf, "peak": DFMA_MEASURED_TFLOPS,
                           "unit": "TFLOP/s", "frac": achieved_tf / DFMA_MEASURED_TFLOPS,
                           "algorithmic_flops_per_launch": flops_launch,
-                          "peak_source": "tools/peaks/fp64_peak.cu DFMA burst (profiles/fp64_peak.json)"},
+                          "peak_source": "tools/peaks/fp64_peak.cu DFMA burst at 1965 MHz (profiles/r02/fp64_peak_with_clocks.txt)"},
     }
     if args.config == 5 or flops_launch / bytes_launch > DFMA_MEASURED_TFLOPS * 1e3 / hbm_gbs:
         # compute-bound by the algorithmic count: the FP64 roofline is the binding one

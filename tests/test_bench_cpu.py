@@ -19,7 +19,7 @@ def test_algorithmic_counts():
     # n = 4: 288 unique pairs, 5120 bytes per element
     assert 3 * 4**3 * 3 // 2 == 288
     assert bench.euler_bytes_per_element(4) == 5120
-    assert bench.euler_flops_per_element(4) == 288 * 63 + 192 * 18 + 64 * 16
+    assert bench.euler_flops_per_element(4) == 288 * 73 + 192 * 18 + 64 * 16
     assert bench.modal_bytes_per_element(6) == 19 * 216 * 8 + 8
 
 
