@@ -95,3 +95,40 @@ def test_burgers_state_validation_and_flux_values():
     const = sf.BurgersState(3, 3, np.full(27, 0.7))
     assert np.abs(sf.time_derivative(const)).max() <= 1e-14
     assert sf.entropy_time_derivative(sf.BurgersState(2, 4, np.zeros(16))) == 0.0
+
+
+def test_c_program_through_the_host_abi(tmp_path):
+    """A plain C11 program (tests/c_abi/host_call.c) calls the host-buffer entry
+    sfb_euler_volume_cartesian_host; its checksum equals the Python device path's
+    on the same inputs and operator."""
+    import os
+    import subprocess
+
+    import torch
+
+    from conftest import ROOT
+    from paper_2306_11665_b200 import _lib
+    from paper_2306_11665_b200 import euler as eu
+
+    exe = tmp_path / "host_call"
+    libdir = os.path.dirname(_lib.LIB_PATH)
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "c_abi", "host_call.c"), "-o", str(exe), "-L",
+                    libdir, "-lsumfac_b200", f"-Wl,-rpath,{libdir}"], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()
+    assert out[0] == "ok"
+    checksum = float(out[2])
+    E, n, nodes = 3, 4, 64
+    D = np.array([-3.0, 4.04508497187474, -1.54508497187474, 0.5,
+                  -0.809016994374947, 0.0, 1.11803398874989, -0.309016994374947,
+                  0.309016994374947, -1.11803398874989, 0.0, 0.809016994374947,
+                  -0.5, 1.54508497187474, -4.04508497187474, 3.0]).reshape(4, 4)
+    U = np.zeros((E, 5, nodes))
+    for e in range(E):
+        for r in range(nodes):
+            rho = 1.0 + 0.01 * ((r * 7 + e) % 11)
+            U[e, 0, r], U[e, 1, r] = rho, rho * 0.05
+            U[e, 4, r] = 1.0 / 0.4 + 0.5 * rho * 0.05 * 0.05
+    R = eu.volume_cartesian(torch.from_numpy(U).cuda(), n, D=D).cpu().numpy()
+    ref = float((R * R).sum())
+    assert abs(checksum - ref) <= 1e-12 * ref

@@ -128,3 +128,16 @@ def test_round2_entries_validate_without_gpu():
     _lib.call("sfb_euler_volume_cartesian_ws", 0, 6, ctypes.addressof(d), 1.4, 2.0, None, None,
               None, None)
     assert _lib.launch_count() == 0
+
+
+def test_header_compiles_and_links_as_plain_c(tmp_path):
+    # the boundary is C: a C11 program includes the header and links the library
+    from paper_2306_11665_b200 import _lib
+
+    src = os.path.join(ROOT, "tests", "c_abi", "host_call.c")
+    exe = tmp_path / "host_call"
+    libdir = os.path.dirname(_lib.LIB_PATH)
+    out = subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                          src, "-o", str(exe), "-L", libdir, "-lsumfac_b200",
+                          f"-Wl,-rpath,{libdir}"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
