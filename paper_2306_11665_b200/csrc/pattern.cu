@@ -196,6 +196,9 @@ __global__ void __launch_bounds__(256) hadamard_rowsum_fixed_kernel(
   }
 }
 
+// LARGE: rows longer than 128 need numpy's recursive split; the n <= 128
+// instantiation carries no recursion (and so no stack / spills)
+template <bool LARGE>
 __global__ void hadamard_rowsum_generic_kernel(int64_t E, int64_t R, int64_t n, int d,
                                                const double* __restrict__ basis,
                                                const double* __restrict__ F,
@@ -211,7 +214,9 @@ __global__ void hadamard_rowsum_generic_kernel(int64_t E, int64_t R, int64_t n, 
       const double* f = F + ((e * d + j) * R + row) * n;
       const double* b = basis + ((int64_t)j * R + row) * n;
       auto ld = [f, b](int64_t i) { return __dmul_rn(b[i], f[i]); };
-      double s = (n <= 128) ? numpy_sum_small(ld, (int)n) : numpy_pairwise_sum(ld, 0, n);
+      double s;
+      if constexpr (LARGE) s = numpy_pairwise_sum(ld, 0, n);
+      else s = numpy_sum_small(ld, (int)n);
       if (out_dir) out_dir[(e * d + j) * R + row] = s;
       acc = (j == 0) ? s : __dadd_rn(acc, s);
     }
@@ -367,8 +372,12 @@ extern "C" int sfb_hadamard_rowsum_batched(int64_t E, int64_t m, int64_t n, int6
     case 93: hadamard_rowsum_fixed_kernel<9, 3><<<blocks, threads, 0, s>>>(E, R, basis, F, out_dir, out_sum); break;
     case 123: hadamard_rowsum_fixed_kernel<12, 3><<<blocks, threads, 0, s>>>(E, R, basis, F, out_dir, out_sum); break;
     default:
-      hadamard_rowsum_generic_kernel<<<grid_for(total, threads), threads, 0, s>>>(
-          E, R, n, (int)d, basis, F, out_dir, out_sum);
+      if (n <= 128)
+        hadamard_rowsum_generic_kernel<false><<<grid_for(total, threads), threads, 0, s>>>(
+            E, R, n, (int)d, basis, F, out_dir, out_sum);
+      else
+        hadamard_rowsum_generic_kernel<true><<<grid_for(total, threads), threads, 0, s>>>(
+            E, R, n, (int)d, basis, F, out_dir, out_sum);
   }
   return check_launch("hadamard_rowsum_batched");
 }
