@@ -26,6 +26,9 @@
 namespace sfb {
 
 // du/dt at node r of the element whose values are v (shared or global).
+// LARGE: n > 128 rows need numpy's recursive split; the other instantiation
+// carries no recursion (no stack frame, no spills).
+template <bool LARGE>
 __device__ __forceinline__ double burgers_dudt_node(int64_t r, int n, int d, int64_t nodes,
                                                     const double* __restrict__ qf,
                                                     const double* __restrict__ omega, int flux,
@@ -39,7 +42,9 @@ __device__ __forceinline__ double burgers_dudt_node(int64_t r, int n, int d, int
     const int64_t base = r - digit * stride;
     const double* q = qf + ((int64_t)j * nodes + r) * n;
     auto ld = [&](int64_t l) { return __dmul_rn(__ldg(q + l), two_point(flux, ur, v[base + l * stride])); };
-    const double s = (n <= 128) ? numpy_sum_small(ld, n) : numpy_pairwise_sum(ld, 0, n);
+    double s;
+    if constexpr (LARGE) s = numpy_pairwise_sum(ld, 0, n);
+    else s = numpy_sum_small(ld, n);
     acc = (j == 0) ? s : __dadd_rn(acc, s);
     stride *= n;
   }
@@ -63,6 +68,7 @@ __device__ __forceinline__ double burgers_dudt_node(int64_t r, int n, int d, int
   return __dadd_rn(vol, surf);
 }
 
+template <bool LARGE>
 __global__ void burgers_dudt_kernel(int64_t E, int n, int d, int64_t nodes,
                                     const double* __restrict__ qf,
                                     const double* __restrict__ omega, int flux, double w0,
@@ -72,7 +78,7 @@ __global__ void burgers_dudt_kernel(int64_t E, int n, int d, int64_t nodes,
   const int64_t total = E * nodes;
   for (; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = t / nodes;
-    dudt[t] = burgers_dudt_node(t - e * nodes, n, d, nodes, qf, omega, flux, w0, wn,
+    dudt[t] = burgers_dudt_node<LARGE>(t - e * nodes, n, d, nodes, qf, omega, flux, w0, wn,
                                 u + e * nodes);
   }
 }
@@ -94,6 +100,7 @@ __device__ __forceinline__ double block_sum_fixed(double x, double* wsum) {
   return t;
 }
 
+template <bool LARGE>
 __global__ void burgers_rk4_kernel(int64_t E, int n, int d, int64_t nodes,
                                    const double* __restrict__ qf,
                                    const double* __restrict__ omega, int flux, double w0,
@@ -128,7 +135,7 @@ __global__ void burgers_rk4_kernel(int64_t E, int n, int d, int64_t nodes,
         if (act) v[r] = (stage == 0) ? ur : v[r];
         __syncthreads();
         const double k =
-            act ? burgers_dudt_node(r, n, d, nodes, qf, omega, flux, w0, wn, v) : 0.0;
+            act ? burgers_dudt_node<LARGE>(r, n, d, nodes, qf, omega, flux, w0, wn, v) : 0.0;
         __syncthreads();  // all reads of this stage's input are done
         if (act) {
           if (stage == 0) sum = k;
@@ -166,7 +173,8 @@ extern "C" int sfb_burgers_time_derivative(int64_t E, int64_t n, int64_t d,
   SFB_CHECK_ARG(qfactors && omega && u && dudt, "null pointer");
   int64_t nodes = 1;
   for (int64_t i = 0; i < d; ++i) nodes *= n;
-  burgers_dudt_kernel<<<grid_cap(E * nodes, 256), 256, 0, (cudaStream_t)stream>>>(
+  auto kern = n <= 128 ? burgers_dudt_kernel<false> : burgers_dudt_kernel<true>;
+  kern<<<grid_cap(E * nodes, 256), 256, 0, (cudaStream_t)stream>>>(
       E, (int)n, (int)d, nodes, qfactors, omega, flux, w0, wn, u, dudt);
   return check_launch("burgers_time_derivative");
 }
@@ -190,7 +198,9 @@ extern "C" int sfb_burgers_rk4(int64_t E, int64_t n, int64_t d, const double* qf
   int64_t grid = E;
   const int64_t cap = (int64_t)num_sms() * (2048 / threads);
   if (grid > cap) grid = cap;
-  burgers_rk4_kernel<<<(unsigned)grid, threads, nodes * sizeof(double), (cudaStream_t)stream>>>(
+  // (nodes <= 1024 implies n <= 1024; rows above 128 only for d = 1)
+  auto kern = n <= 128 ? burgers_rk4_kernel<false> : burgers_rk4_kernel<true>;
+  kern<<<(unsigned)grid, threads, nodes * sizeof(double), (cudaStream_t)stream>>>(
       E, (int)n, (int)d, nodes, qfactors, omega, flux, w0, wn, dt, (int)steps, (int)every, u,
       entropy, mass);
   return check_launch("burgers_rk4");

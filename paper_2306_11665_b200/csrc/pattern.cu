@@ -124,13 +124,15 @@ __global__ void hadamard_evaluate_kernel(const double* __restrict__ a,
   for (; t < count; t += (int64_t)gridDim.x * blockDim.x) out[t] = __dmul_rn(a[t], b[t]);
 }
 
+template <bool LARGE>  // n > 128: numpy's recursive split (the other has no stack)
 __global__ void row_sum_kernel(const double* __restrict__ p, int64_t rows, int64_t n,
                                double* __restrict__ out) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   for (; t < rows; t += (int64_t)gridDim.x * blockDim.x) {
     const double* row = p + t * n;
     auto ld = [row](int64_t i) { return row[i]; };
-    out[t] = (n <= 128) ? numpy_sum_small(ld, (int)n) : numpy_pairwise_sum(ld, 0, n);
+    if constexpr (LARGE) out[t] = numpy_pairwise_sum(ld, 0, n);
+    else out[t] = numpy_sum_small(ld, (int)n);
   }
 }
 
@@ -228,6 +230,7 @@ __global__ void hadamard_rowsum_generic_kernel(int64_t E, int64_t R, int64_t n, 
 // Scalar Burgers flux differencing, fused (burgers.py:117-131):
 // out[e,r] = (-2.0 * sum_j rowsum_j[r]) / omega[r]
 // --------------------------------------------------------------------------
+template <bool LARGE>
 __global__ void burgers_volume_kernel(int64_t E, int64_t n, int d, int64_t nodes,
                                       const double* __restrict__ qf,
                                       const double* __restrict__ omega, int flux,
@@ -246,7 +249,9 @@ __global__ void burgers_volume_kernel(int64_t E, int64_t n, int d, int64_t nodes
       int64_t base = r - digit * stride;
       const double* q = qf + ((int64_t)j * nodes + r) * n;
       auto ld = [&](int64_t l) { return __dmul_rn(q[l], two_point(flux, ur, ue[base + l * stride])); };
-      double s = (n <= 128) ? numpy_sum_small(ld, (int)n) : numpy_pairwise_sum(ld, 0, n);
+      double s;
+      if constexpr (LARGE) s = numpy_pairwise_sum(ld, 0, n);
+      else s = numpy_sum_small(ld, (int)n);
       acc = (j == 0) ? s : __dadd_rn(acc, s);
       stride *= n;
     }
@@ -338,7 +343,8 @@ extern "C" int sfb_hadamard_row_sum(const double* product, int64_t rows, int64_t
   SFB_CHECK_ARG(rows >= 0 && n >= 1, "bad extents");
   if (rows == 0) return SFB_OK;
   SFB_CHECK_ARG(product && out, "null pointer");
-  row_sum_kernel<<<grid_for(rows, 256), 256, 0, (cudaStream_t)stream>>>(product, rows, n, out);
+  auto kern = n <= 128 ? row_sum_kernel<false> : row_sum_kernel<true>;
+  kern<<<grid_for(rows, 256), 256, 0, (cudaStream_t)stream>>>(product, rows, n, out);
   return check_launch("hadamard_row_sum");
 }
 
@@ -392,7 +398,8 @@ extern "C" int sfb_burgers_volume(int64_t E, int64_t n, int64_t d, const double*
   int64_t nodes = 1;
   for (int64_t i = 0; i < d; ++i) nodes *= n;
   int64_t total = E * nodes;
-  burgers_volume_kernel<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
+  auto kern = n <= 128 ? burgers_volume_kernel<false> : burgers_volume_kernel<true>;
+  kern<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
       E, n, (int)d, nodes, qfactors, omega, flux, u, out);
   return check_launch("burgers_volume");
 }
