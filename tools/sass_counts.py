@@ -10,7 +10,7 @@ LIB = sys.argv[1] if len(sys.argv) > 1 else "paper_2306_11665_b200/libsumfac_b20
 KEYS = ["UBLKCP", "UBLKPF", "LDGSTS", "SYNCS", "STL", "LDL", "DFMA", "DMUL", "DADD", "MUFU",
         "SHFL", "LDS", "STS", "LDG", "STG", "BAR", "DMMA"]
 HOT = ["euler_cart_own_kernel", "euler_cart_sync_kernel", "euler_cartesian_kernel",
-       "euler_cart_node_kernel", "euler_modal_kernel", "hadamard_rowsum_fixed_kernel",
+       "euler_cart_node_kernel", "euler_cart_n2_kernel", "euler_cart_n3_kernel", "euler_modal_kernel", "hadamard_rowsum_fixed_kernel",
        "hadamard_rowsum_generic_kernel", "burgers_rk4"]
 
 out = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
