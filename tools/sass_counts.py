@@ -32,5 +32,5 @@ for name, c in funcs.items():
     dem = subprocess.run(["c++filt", name], capture_output=True, text=True).stdout.strip()
     if not any(h in dem for h in HOT):
         continue
-    short = dem.split("(")[0].replace("sfb::", "")
+    short = dem.replace("(anonymous namespace)::", "").split("(")[0].replace("sfb::", "")
     print(f"{short} | " + " | ".join(str(c.get(k, 0)) for k in KEYS) + f" | {sum(c.values())}")
