@@ -446,6 +446,10 @@ def run_ours(args):
         # path on a one-GPU box (never for reported numbers)
         backend = os.environ.get("SFB_DIST_BACKEND", "nccl")
         if backend == "nccl":
+            # NCCL's init lines (communicator size, transport) on stderr: the
+            # rank count stays observable outside the JSON line too
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
@@ -495,6 +499,7 @@ def run_ours(args):
         elif world > 1 and not args.no_extras:
             line["config5_sharded"] = sharded_config5(args, world, rank, dev, stream, sampler,
                                                       dist)
+            line["comm_nranks"] = line["config5_sharded"]["comm_nranks"]
     sampler.stop()
     if rank == 0:
         print(json.dumps(line), flush=True)
